@@ -1,0 +1,166 @@
+/*
+ * loza.h — C ABI of libloza.so, the B200 (sm_100a) hot path of LoZA
+ * (LongCat ZigZag Attention, arXiv 2512.23966): streaming sparse attention (SSA)
+ * over the absorbed latent MLA key/value cache, its full-attention comparator,
+ * and the LoZA calibration blend.
+ *
+ * Notation (Eq. 1-4):
+ *   B batch, n_q query tokens, n_kv key tokens, H query heads, one shared latent
+ *   KV head (MLA), d_qk = 512 latent + 64 RoPE = 576, d_v = 512
+ *   (V = the first d_v columns of the latent KV row; pass v == k).
+ *   Pattern (s, l, b) = (#sink blocks, #local blocks, block size), PAPER.md:57;
+ *   paper default (1, 7, 128) = 1,024-token window.
+ *   Query at absolute position p attends key j  <=>  j <= p and
+ *   ( floor(j/b) < s  or  floor(p/b) - floor(j/b) < l ).
+ *   The query's own (partial) block is one of the l local blocks (DESIGN R2).
+ *
+ * Conventions shared by every entry point:
+ *   - All pointers named *_dev / q / k / v / o / lse / ws are DEVICE pointers;
+ *     the caller owns every buffer; the library never allocates device memory
+ *     (workspace sizes are queried with loza_workspace_size).
+ *   - Every call is asynchronous on `stream` (a cudaStream_t passed as void*,
+ *     NULL = legacy default stream) and never synchronises the host. seq_lens,
+ *     alpha and d_alpha live on the device, so decode and blend steps are
+ *     CUDA-graph capturable.
+ *   - Strides are in ELEMENTS. Offsets are int64 (a 1M-token Q has 3.9e10 elems).
+ *   - Errors: host-side validation happens before any launch and returns a
+ *     status; nothing is launched on error. LOZA_ERR_CUDA / LOZA_ERR_NCCL carry
+ *     text in loza_last_error() (thread-local). No exceptions cross the ABI.
+ *     There is NO fallback path: an unsupported combination returns
+ *     LOZA_ERR_UNSUPPORTED.
+ *   - Dispatch: in_dtype LOZA_F32 -> SIMT fp32 kernels (any d_qk <= 576,
+ *     d_v <= 512, any b >= 1); in_dtype LOZA_BF16 with (d_qk, d_v) = (576, 512)
+ *     and b % 128 == 0 -> tcgen05/TMEM/TMA kernels. Anything else: UNSUPPORTED.
+ */
+#ifndef LOZA_H_
+#define LOZA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* loza_stream_t;     /* cudaStream_t */
+typedef void* loza_nccl_comm_t;  /* ncclComm_t (NCCL 2.28, the libnccl.so.2 torch loads) */
+
+typedef enum {
+  LOZA_OK = 0,
+  LOZA_ERR_INVALID = 1,      /* bad pattern / scale / flags / alpha */
+  LOZA_ERR_SHAPE = 2,        /* inconsistent dims or strides, misalignment, n_kv < q_start + n_q */
+  LOZA_ERR_UNSUPPORTED = 3,  /* valid but not implemented on this path (no fallback) */
+  LOZA_ERR_CUDA = 4,
+  LOZA_ERR_NCCL = 5
+} loza_status_t;
+
+typedef enum { LOZA_F32 = 0, LOZA_BF16 = 1 } loza_dtype_t;
+
+/* Sparse pattern of Eq. 4: s >= 0, l >= 1, b >= 1. */
+typedef struct {
+  int32_t sink_blocks;   /* s */
+  int32_t local_blocks;  /* l (includes the query's own block) */
+  int32_t block_size;    /* b */
+} loza_pattern_t;
+
+/* One attention problem. Q row (batch, i, head) sits at absolute position
+ * q_start + i and attends keys [0, n_kv) of its batch under the mask. */
+typedef struct {
+  int32_t batch, n_q, heads, d_qk, d_v;
+  int64_t n_kv;          /* keys available per batch (prefill: >= q_start + n_q) */
+  int64_t q_start;       /* absolute position of query row 0 (multiple of b for SSA) */
+  loza_dtype_t in_dtype;   /* q, k, v */
+  loza_dtype_t out_dtype;  /* o (bf16 RN-even or fp32) */
+  float softmax_scale;   /* logits = softmax_scale * q.k (Eq. 1 "details omitted": DESIGN R1) */
+  int32_t causal;        /* 1 = causal (required by SSA), 0 = bidirectional (full_attn_ref only) */
+  const void* q; int64_t q_stride_b, q_stride_tok, q_stride_head;  /* [B, n_q, H, d_qk] */
+  const void* k; int64_t k_stride_b, k_stride_tok;                 /* [B, n_kv, d_qk] latent, 1 KV head */
+  const void* v; int64_t v_stride_b, v_stride_tok;                 /* [B, n_kv, d_v]; MLA: v == k */
+  void* o;       int64_t o_stride_b, o_stride_tok, o_stride_head;  /* [B, n_q, H, d_v] */
+  float* lse;    /* optional [B, H, n_q] fp32, natural log: m + ln(sum) ; NULL = skip */
+} loza_attn_args_t;
+
+/* SSA prefill, Eq. 4: O* = softmax(scale Q K*^T) V* with K*, V*
+ * the sink + local blocks of each query block. Causal only (causal = 0 returns
+ * LOZA_ERR_UNSUPPORTED, DESIGN R9). bf16 path: q/o rows must be head-contiguous
+ * (q_stride_head == d_qk, q_stride_tok == H*d_qk, same for o), H*b % 128 == 0. */
+loza_status_t ssa_prefill(const loza_attn_args_t* args, loza_pattern_t pattern, loza_stream_t stream);
+
+/* SSA decode (one new token per sequence), Eq. 4 with the query at position
+ * p = seq_lens[b] - 1 (seq_len INCLUDES the current token, DESIGN R8): reads only
+ * the sink block(s) and the last l blocks of the cache, so its cost is
+ * independent of the context length. args->n_q must be 1; args->n_kv = cache
+ * capacity T_cap; seq_lens_dev [B] int32 on the device, 1 <= seq_len <= T_cap
+ * (out-of-range values are clamped on the device). q [B,1,H,d_qk] -> o [B,1,H,d_v].
+ * ws: loza_workspace_size(LOZA_WS_DECODE, ...) bytes (may be 0 -> ws NULL). */
+loza_status_t ssa_decode(const loza_attn_args_t* args, const int32_t* seq_lens_dev,
+                         loza_pattern_t pattern, void* ws, size_t ws_bytes, loza_stream_t stream);
+
+/* Full-attention comparator, Eq. 1 with a causal (or, for
+ * causal = 0, bidirectional) mask. seq_lens_dev == NULL: prefill over
+ * [q_start, q_start + n_q); otherwise decode as in ssa_decode over the whole
+ * context [0, seq_len). ws sized by loza_workspace_size(LOZA_WS_FULL_DECODE, ...). */
+loza_status_t full_attn_ref(const loza_attn_args_t* args, const int32_t* seq_lens_dev, void* ws,
+                            size_t ws_bytes, loza_stream_t stream);
+
+/* LoZA calibration blend, Eq. 3:
+ *   o_hat = alpha * o_full + (1 - alpha) * o_sparse, evaluated as
+ *   fma(alpha, o_full, (1-alpha) * o_sparse) in fp32 so alpha in {0, 1} is exact,
+ * and, if d_o_hat and d_alpha_dev are non-NULL, the scalar gradient
+ *   d_alpha = sum_e d_o_hat[e] * (o_full[e] - o_sparse[e])
+ * (per-thread fp32, per-CTA fp64, final fixed-order fp64 sum: deterministic).
+ * All arrays contiguous, numel elements of `dtype`; alpha_dev one device fp32.
+ * o_hat may be NULL (gradient only). If alpha is NaN or outside [0, 1] the kernel
+ * writes LOZA_ERR_INVALID to status_dev (if non-NULL) and NaN to d_alpha
+ * (out-of-range alpha is a contract error); otherwise it writes
+ * LOZA_OK to status_dev. ws: loza_workspace_size(LOZA_WS_BLEND, ...) bytes,
+ * required when d_alpha_dev != NULL. numel must be a multiple of 8 and
+ * pointers 16-byte aligned (LOZA_ERR_SHAPE). */
+loza_status_t loza_blend(const void* o_full, const void* o_sparse, const float* alpha_dev, void* o_hat,
+                         const void* d_o_hat, double* d_alpha_dev, int64_t numel, loza_dtype_t dtype,
+                         int32_t* status_dev, void* ws, size_t ws_bytes, loza_stream_t stream);
+
+/* Sequence-parallel SSA prefill (north star; "uniform compute across
+ * all ranks"). Rank r of `world` owns the contiguous, block-aligned shard of one
+ * sequence at positions [q_start, q_start + n_local) with n_local = args->n_q,
+ * q_start = r * n_local (equal shards), and k/v holding exactly the shard's own
+ * rows (args->n_kv == n_local; k row 0 = position q_start; rows contiguous).
+ * One NCCL group on `stream`: rank 0 broadcasts its first s*b KV rows (the sink
+ * blocks), rank r sends its last (l-1)*b KV rows to rank r+1 and receives the
+ * halo from rank r-1; then the SSA prefill of the shard runs over the segmented
+ * KV [sink | halo | shard]. The output stays sharded (o/lse hold the shard's rows).
+ * Requires n_local % b == 0 and n_local >= max(s, l-1) * b (LOZA_ERR_SHAPE).
+ * `comm` (an ncclComm_t of `world` ranks) may be NULL when world == 1.
+ * ws: loza_workspace_size(LOZA_WS_SEQPAR, args, pattern, world) bytes. */
+loza_status_t ssa_seqpar_prefill(const loza_attn_args_t* args, loza_pattern_t pattern, loza_nccl_comm_t comm,
+                                 int32_t rank, int32_t world, void* ws, size_t ws_bytes, loza_stream_t stream);
+
+/* Test hook ("virtual ranks"): ssa_seqpar_prefill with the NCCL exchange replaced
+ * by device-to-device copies from the other shards' k/v on this GPU (rank0_k/v:
+ * rank 0's shard base; prev_k/v: rank r-1's shard base; ignored for rank 0). */
+loza_status_t loza_seqpar_prefill_local(const loza_attn_args_t* args, loza_pattern_t pattern, int32_t rank,
+                                        int32_t world, const void* rank0_k, const void* rank0_v,
+                                        const void* prev_k, const void* prev_v, void* ws, size_t ws_bytes,
+                                        loza_stream_t stream);
+
+/* Test hook for the integer prologue: for the query blocks of
+ * queries [q_start, q_start + n_q) (q_start % b == 0), local block qb:
+ *   idx_dev[qb*(s+l) + t] = t-th selected key block (absolute, ascending), -1 padded;
+ *   count_dev[qb] = |sel| = number of selected key blocks.
+ * sel(QB) = {kb <= QB : kb < s or QB - kb < l} (closed form of the mask). */
+loza_status_t ssa_select_blocks(int64_t n_q, int64_t q_start, loza_pattern_t pattern, int32_t causal,
+                                int32_t* idx_dev, int32_t* count_dev, loza_stream_t stream);
+
+enum { LOZA_WS_DECODE = 0, LOZA_WS_FULL_DECODE = 1, LOZA_WS_BLEND = 2, LOZA_WS_SEQPAR = 3 };
+/* Workspace bytes for `which`; args may be NULL for LOZA_WS_BLEND. */
+size_t loza_workspace_size(int32_t which, const loza_attn_args_t* args, loza_pattern_t pattern, int32_t world);
+
+const char* loza_status_string(loza_status_t status);
+const char* loza_last_error(void);           /* thread-local text of the last error, "" if none */
+uint64_t loza_kernel_launches(void);         /* number of library kernel launches so far (process) */
+int32_t loza_num_sms(void);                  /* SM count of the current device (0 if unknown) */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOZA_H_ */

@@ -65,11 +65,15 @@ def fill_(t, spec: Spec, row_start: int = 0) -> None:
         raise RuntimeError(f"loza_gen_fill failed with code {rc}")
 
 
-def empty_filled(spec: Spec, device="cuda"):
-    """Allocate [batch, n, heads, d] on the device and fill it from the generator."""
+def empty_filled(spec: Spec, device="cuda", four_d: bool | None = None):
+    """Allocate the tensor on the device and fill it from the generator: [batch, n, heads, d] for query-like
+    tensors (heads > 1 or tensor_id == TID_Q), else [batch, n, d]."""
     import torch
+    from .gen import TID_Q
     dt = torch.bfloat16 if spec.dtype == "bf16" else torch.float32
-    shape = (spec.batch, spec.n, spec.heads, spec.d) if spec.heads > 1 else (spec.batch, spec.n, spec.d)
+    if four_d is None:
+        four_d = spec.heads > 1 or spec.tensor_id == TID_Q
+    shape = (spec.batch, spec.n, spec.heads, spec.d) if four_d else (spec.batch, spec.n, spec.d)
     t = torch.empty(shape, dtype=dt, device=device)
     fill_(t, spec)
     return t

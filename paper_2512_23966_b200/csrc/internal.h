@@ -1,0 +1,64 @@
+// Internal (non-ABI) declarations of libloza.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/loza.h"
+
+namespace loza {
+
+// A key/value sequence as up to 3 position-contiguous segments (plain prefill:
+// one segment; sequence-parallel prefill: [sink | halo | shard]). Key at
+// absolute position j lives in the segment with pos_begin <= j < pos_end, at
+// row (j - pos_begin) of that segment.
+struct KvSeg {
+  int64_t pos_begin, pos_end;
+  const void* k;
+  const void* v;
+  int64_t k_sb, k_st, v_sb, v_st;  // batch / token strides (elements)
+};
+struct KvView {
+  int32_t nseg;
+  KvSeg seg[3];
+};
+
+struct AttnProblem {
+  int32_t batch, n_q, heads, d_qk, d_v;
+  int64_t n_kv, q_start;
+  int32_t in_bf16, out_bf16;
+  float scale;
+  int32_t causal, sparse;
+  int32_t s, l, b;
+  const void* q;
+  int64_t q_sb, q_st, q_sh;
+  void* o;
+  int64_t o_sb, o_st, o_sh;
+  float* lse;
+  const int32_t* seq_lens;  // non-NULL => decode (one query at seq_len-1)
+  KvView kv;
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_select_blocks(int64_t n_q, int64_t q_start, int32_t s, int32_t l, int32_t b,
+                                 int32_t* idx, int32_t* cnt, cudaStream_t st);
+cudaError_t launch_attn_simt(const AttnProblem& p, cudaStream_t st);
+cudaError_t launch_blend(const void* o_full, const void* o_sparse, const float* alpha, void* o_hat,
+                         const void* d_o_hat, double* d_alpha, int64_t numel, int bf16, int32_t* status,
+                         void* ws, cudaStream_t st);
+size_t blend_ws_bytes();
+// tcgen05 paths (bf16, d_qk 576, d_v 512)
+cudaError_t launch_prefill_tc(const AttnProblem& p, cudaStream_t st);
+cudaError_t launch_decode_tc(const AttnProblem& p, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t decode_tc_ws_bytes(const AttnProblem& p);
+
+void count_launch(uint64_t n = 1);
+loza_status_t fail(loza_status_t st, const char* fmt, ...);
+loza_status_t cuda_status(cudaError_t e, const char* what);
+loza_status_t make_problem(const loza_attn_args_t* a, bool sparse, loza_pattern_t pat, const int32_t* seq_lens,
+                           AttnProblem* p);
+loza_status_t run_attention(const loza_attn_args_t* a, const AttnProblem& p, void* ws, size_t ws_bytes,
+                            cudaStream_t st);
+int device_sm_count();
+
+}  // namespace loza
