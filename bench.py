@@ -1,0 +1,461 @@
+"""Benchmark of the LoZA SSA hot path on B200 (BASELINE.json metric: SSA prefill & decode tokens/s, % roofline).
+
+Contract (one JSON line on rank 0):
+  N=1 : headline workload = BASELINE.json configs[1]: SSA prefill, B1 H64 n32768, MLA-absorbed (576/512),
+        (s,l,b) = (1,7,128), bf16 in / fp32 accumulate / bf16 out; value = tokens/s. The other §8 rows
+        (full-attention comparator at the same shape, decode B64 at 128K/512K/1M, blend 8K) are measured in
+        the same run and reported under "rows".
+  N>1 : sequence-parallel SSA prefill (configs[4] path): each rank owns a 32768-token shard of one
+        (32768*N)-token sequence, NCCL halo + sink exchange; weak scaling; value = total tokens / max-rank time.
+  --impl reference : the fp64 CPU oracle (oracle/) timed on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PATTERN = (1, 7, 128)
+D_QK, D_V, H = 576, 512, 64
+N_PREFILL = 32768
+FLOP_PER_PAIR = 2 * (D_QK + D_V) * H  # 139,264
+
+
+def ssa_pairs(n, s, l, b, q_start=0):
+    """Unmasked (query, key) pairs of SSA for queries [q_start, q_start+n) (closed form summed per block)."""
+    tot = 0
+    for qb in range(q_start // b, (q_start + n + b - 1) // b):
+        lo, hi = max(qb * b, q_start), min((qb + 1) * b, q_start + n)
+        sink_blocks = [kb for kb in range(min(s, qb + 1))]
+        loc = [kb for kb in range(max(s, qb - l + 1), qb + 1)]
+        for p in range(lo, hi):
+            cnt = 0
+            for kb in sink_blocks + loc:
+                cnt += max(0, min((kb + 1) * b, p + 1) - kb * b)
+            tot += cnt
+    return tot
+
+
+def full_pairs(n):
+    return n * (n + 1) // 2
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained"), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def _time_events(fn, iters, warmup, flush=None, stream=None):
+    """Per-iteration device times (ms) with CUDA events on the launching stream; L2 flushed between iterations."""
+    import torch
+    stream = stream or torch.cuda.current_stream()
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(iters):
+        if flush is not None:
+            flush()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        fn()
+        e.record(stream)
+        e.synchronize()
+        times.append(s.elapsed_time(e))
+    return times
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from inputs import TID_K, TID_Q, Spec
+    from inputs.device import empty_filled, fill_
+    from paper_2512_23966_b200 import loza
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = measured_peaks()
+    scale = loza.default_scale(D_QK)
+    s, l, b = PATTERN
+    n_local = N_PREFILL
+    n_total = n_local * world
+
+    # inputs (generated on the device; seed 0, D1 distribution)
+    qs = Spec(seed=0, tensor_id=TID_Q, batch=1, n=n_total, heads=H, d=D_QK)
+    ks = Spec(seed=0, tensor_id=TID_K, batch=1, n=n_total, heads=1, d=D_QK)
+    q = torch.empty((1, n_local, H, D_QK), dtype=torch.bfloat16, device=dev)
+    kv = torch.empty((1, n_local, D_QK), dtype=torch.bfloat16, device=dev)
+    fill_(q, qs, row_start=rank * n_local * H)
+    fill_(kv, ks, row_start=rank * n_local)
+    o = torch.empty((1, n_local, H, D_V), dtype=torch.bfloat16, device=dev)
+    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def flush():
+        flush_buf.fill_(1)
+
+    comm_ptr = 0
+    if world > 1:
+        pg = dist.group.WORLD
+        dist.barrier()
+        backend = pg._get_backend(dev)
+        comm_ptr = backend._comm_ptr()
+    ws = None
+    if world > 1:
+        need = loza.seqpar_ws_bytes(q, kv, kv[..., :D_V], PATTERN, world)
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+
+    def step():
+        if world == 1:
+            loza.ssa_prefill(q, kv, pattern=PATTERN, scale=scale, out=o)
+        else:
+            loza.ssa_seqpar_prefill(q, kv, pattern=PATTERN, scale=scale, rank=rank, world=world, comm_ptr=comm_ptr,
+                                    out=o, ws=ws)
+
+    # ---- headline: K timed steps bracketed by barrier + sync, max over ranks
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = loza.kernel_launches()
+    per_step = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            step()
+            ev1.record()
+            ev1.synchronize()
+            per_step.append(ev0.elapsed_time(ev1))
+        torch.cuda.synchronize()
+    launches = loza.kernel_launches() - launches0
+    t_ms = float(np.mean(per_step))
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    tokens = n_total
+    value = tokens / (t_ms * 1e-3)
+    pairs = ssa_pairs(n_local, s, l, b, q_start=rank * n_local)
+    flops = pairs * FLOP_PER_PAIR
+    achieved_tf = flops / (float(np.mean(per_step)) * 1e-3) / 1e12
+
+    rows = {}
+    if rank == 0 and world == 1 and not args.quick:
+        rows = extra_rows(args, q, kv, o, flush, peaks)
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        qh = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+        kh = torch.empty(kv.shape, dtype=kv.dtype, pin_memory=True)
+        oh = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
+        qh.copy_(q)
+        kh.copy_(kv)
+        qd = torch.empty_like(q)
+        kd = torch.empty_like(kv)
+
+        def e2e_step():
+            qd.copy_(qh, non_blocking=True)
+            kd.copy_(kh, non_blocking=True)
+            loza.ssa_prefill(qd, kd, pattern=PATTERN, scale=scale, out=o)
+            oh.copy_(o, non_blocking=True)
+        ts = _time_events(e2e_step, max(2, args.steps // 2), 1)
+        e2e = {"value": n_local / (float(np.mean(ts)) * 1e-3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(q.numel() * 2 + kv.numel() * 2), "d2h_bytes_per_step": int(o.numel() * 2),
+               "ms_per_step": float(np.mean(ts))}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.cpu_seconds)
+
+    if rank == 0:
+        frac = achieved_tf / peaks["bf16_tflops"]
+        line = {
+            "metric": "SSA prefill tokens/s (B1 H64 n32768 MLA 576/512, (s,l,b)=(1,7,128)); % tensor roofline",
+            "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (counter-based N(0,1)-like, seed 0; inputs/gen.py)",
+            "config": {"workload": "ssa_prefill_32k" if world == 1 else f"ssa_seqpar_prefill_{world}x32k",
+                       "batch": 1, "seq_len": n_total, "tokens_per_gpu": n_local, "heads": H, "d_qk": D_QK,
+                       "d_v": D_V, "pattern": list(PATTERN), "softmax_scale": scale,
+                       "parallelism": f"sp{world}" if world > 1 else "single",
+                       "l2": "flushed between timed steps (256 MB write)"},
+            "roofline": {"bound": "tensor", "kernel": "prefill_tc_kernel", "achieved": achieved_tf,
+                         "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": frac, "traffic": None,
+                         "algorithmic_flop_per_launch": flops, "pairs_per_launch": pairs,
+                         "peak_source": peaks["source"] + " bf16_tflops (burst)",
+                         "frac_vs_sustained": achieved_tf / peaks["bf16_tflops_sustained"]
+                         if peaks.get("bf16_tflops_sustained") else None},
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "rows": rows,
+            "paper_context": {"decode_ssa_vs_flashmla_128k": ">=90% less cost (PAPER.md:244, hardware unstated)",
+                              "e2e_prefill_speedup_256k": ">50% (PAPER.md:244)",
+                              "e2e_decode_saving_256k": ">30% (PAPER.md:244)"},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def extra_rows(args, q, kv, o, flush, peaks):
+    """The other §8 rows, each with its own roofline: full prefill comparator, decode (128K/512K/1M), blend 8K."""
+    import torch
+
+    from inputs import TID_DO, TID_K, TID_Q, Spec
+    from inputs.device import fill_
+    from paper_2512_23966_b200 import loza
+    out = {}
+    scale = loza.default_scale(D_QK)
+    dev = q.device
+    # full-attention prefill at the same shape
+    t = _time_events(lambda: loza.full_attn_ref(q, kv, scale=scale, out=o), 2, 1, flush)
+    fl = full_pairs(N_PREFILL) * FLOP_PER_PAIR
+    tf = fl / (float(np.mean(t)) * 1e-3) / 1e12
+    out["full_prefill_32k"] = {"ms": float(np.mean(t)), "tokens_per_s": N_PREFILL / (np.mean(t) * 1e-3),
+                               "tflops": tf, "frac_tensor": tf / peaks["bf16_tflops"]}
+    # blend at 8K (configs[2]): full + SSA forward, blend + d_alpha
+    n8 = 8192
+    q8, kv8 = q[:, :n8], kv[:, :n8]
+    of = torch.empty((1, n8, H, D_V), dtype=torch.bfloat16, device=dev)
+    osp = torch.empty_like(of)
+    dh = torch.empty_like(of)
+    fill_(dh, Spec(seed=0, tensor_id=TID_DO, batch=1, n=n8, heads=H, d=D_V))
+    alpha = torch.tensor([0.5], device=dev)
+    oh = torch.empty_like(of)
+    dal = torch.empty(1, dtype=torch.float64, device=dev)
+    t_full = _time_events(lambda: loza.full_attn_ref(q8, kv8, scale=scale, out=of), 3, 1, flush)
+    t_ssa = _time_events(lambda: loza.ssa_prefill(q8, kv8, pattern=PATTERN, scale=scale, out=osp), 5, 2, flush)
+    t_bl = _time_events(lambda: loza.loza_blend(of, osp, alpha, dh, out=oh, d_alpha=dal), 10, 3, flush)
+    bl_bytes = of.numel() * 2 * 4
+    out["blend_8k"] = {"full_ms": float(np.mean(t_full)), "ssa_ms": float(np.mean(t_ssa)),
+                       "blend_ms": float(np.mean(t_bl)),
+                       "blend_gbs": bl_bytes / (np.mean(t_bl) * 1e-3) / 1e9,
+                       "blend_frac_hbm": bl_bytes / (np.mean(t_bl) * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                       "ssa_frac_tensor": ssa_pairs(n8, *PATTERN) * FLOP_PER_PAIR / (np.mean(t_ssa) * 1e-3) / 1e12
+                       / peaks["bf16_tflops"],
+                       "full_frac_tensor": full_pairs(n8) * FLOP_PER_PAIR / (np.mean(t_full) * 1e-3) / 1e12
+                       / peaks["bf16_tflops"]}
+    del of, osp, dh, oh
+    # decode B64 at 128K / 512K / 1M (configs[3])
+    if not args.no_decode:
+        try:
+            out["decode"] = decode_rows(args, peaks, flush)
+        except Exception as e:  # report, do not hide: the headline line still prints
+            out["decode"] = {"error": repr(e)[:300]}
+    return out
+
+
+def decode_rows(args, peaks, flush):
+    import torch
+
+    from inputs import TID_K, TID_Q, Spec
+    from inputs.device import fill_
+    from paper_2512_23966_b200 import loza
+    dev = torch.device("cuda", torch.cuda.current_device())
+    B = 64
+    free = torch.cuda.mem_get_info()[0]
+    t_cap = 1 << 20
+    while B * t_cap * D_QK * 2 > free * 0.8 and t_cap > (1 << 17):
+        t_cap //= 2
+    cache = torch.empty((B, t_cap, D_QK), dtype=torch.bfloat16, device=dev)
+    fill_(cache, Spec(seed=0, tensor_id=TID_K, batch=B, n=t_cap, heads=1, d=D_QK))
+    qd = torch.empty((B, 1, H, D_QK), dtype=torch.bfloat16, device=dev)
+    fill_(qd, Spec(seed=1, tensor_id=TID_Q, batch=B, n=1, heads=H, d=D_QK))
+    od = torch.empty((B, 1, H, D_V), dtype=torch.bfloat16, device=dev)
+    scale = loza.default_scale(D_QK)
+    res = {}
+    ws = None
+    for ctx in (131072, 524288, 1048576):
+        if ctx > t_cap:
+            continue
+        seq = torch.full((B,), ctx, dtype=torch.int32, device=dev)
+        step = lambda: loza.ssa_decode(qd, cache, seq, pattern=PATTERN, scale=scale, out=od)  # noqa: E731
+        t = _time_events(step, 50, 5, flush)
+        window = min(ctx, (PATTERN[0] + PATTERN[1]) * PATTERN[2])
+        by = B * (window * D_QK * 2 + H * D_QK * 2 + H * D_V * 2)
+        ms = float(np.median(t))
+        tf = lambda: loza.full_attn_ref(qd, cache, scale=scale, seq_lens=seq, out=od)  # noqa: E731
+        tfull = _time_events(tf, 3, 1, flush)
+        by_full = B * (ctx * D_QK * 2 + H * D_QK * 2 + H * D_V * 2)
+        res[str(ctx)] = {"ssa_us": ms * 1e3, "ssa_tokens_per_s": B / (ms * 1e-3), "ssa_gbs": by / (ms * 1e-3) / 1e9,
+                         "ssa_frac_hbm": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "ssa_bytes": by, "full_ms": float(np.mean(tfull)),
+                         "full_gbs": by_full / (np.mean(tfull) * 1e-3) / 1e9,
+                         "full_frac_hbm": by_full / (np.mean(tfull) * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "ssa_cost_vs_full": ms / float(np.mean(tfull))}
+    del cache
+    return res
+
+
+# ----------------------------------------------------------------------------- CPU oracle arm
+def cpu_baseline(seconds: float = 15.0):
+    """The fp64 oracle, as it stands, on a bounded sample of the headline workload: all 64 heads of a set of
+    query tokens spread over the 32K sequence (SSA, (1,7,128)). Returns tokens/s of the oracle."""
+    import oracle
+    from inputs import TID_K, TID_Q, Spec, gen_rows_f32
+    qs = Spec(seed=0, tensor_id=TID_Q, batch=1, n=N_PREFILL, heads=H, d=D_QK)
+    ks = Spec(seed=0, tensor_id=TID_K, batch=1, n=N_PREFILL, heads=1, d=D_QK)
+    kf = gen_rows_f32(ks, 0, N_PREFILL)
+    vf = np.ascontiguousarray(kf[:, :D_V])
+    rng = np.random.default_rng(0)
+    done, t0 = 0, time.perf_counter()
+    spent = 0.0
+    while spent < seconds:
+        toks = np.sort(rng.integers(0, N_PREFILL, 8))
+        for t in toks:
+            qr = gen_rows_f32(qs, int(t) * H, H)
+            ta = time.perf_counter()
+            oracle.attention_rows(qr, np.full(H, int(t)), kf, vf, loza_scale(), *PATTERN)
+            spent += time.perf_counter() - ta
+            done += 1
+    wall = time.perf_counter() - t0
+    return {"value": done / spent, "unit": "tokens/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{done} random query tokens x 64 heads of the 32K SSA prefill (fp64, OpenMP over rows); "
+                      f"{spent:.1f} s of oracle time ({wall:.1f} s wall incl. input regeneration)",
+            "cpu_model": _cpu_model()}
+
+
+def loza_scale():
+    return 1.0 / math.sqrt(192.0)
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    per = []
+    cb = None
+    for _ in range(args.warmup):
+        cpu_baseline(min(2.0, args.cpu_seconds))
+    for _ in range(args.steps):
+        cb = cpu_baseline(args.cpu_seconds / max(1, args.steps) * 2)
+        per.append(cb["value"])
+    value = float(np.mean(per))
+    line = {"impl": "reference",
+            "metric": "SSA prefill tokens/s (B1 H64 n32768 MLA 576/512, (s,l,b)=(1,7,128)); % tensor roofline",
+            "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (counter-based, seed 0)",
+            "config": {"workload": "ssa_prefill_32k", "batch": 1, "seq_len": N_PREFILL, "heads": H,
+                       "pattern": list(PATTERN)},
+            "cpu_baseline": {"kind": "oracle", "cores": cb["cores"], "sample": cb["sample"], "value": value,
+                             "unit": "tokens/s"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--quick", action="store_true", help="headline only (no extra rows)")
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

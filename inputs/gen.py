@@ -130,8 +130,14 @@ def bf16_bits_to_f32(u: np.ndarray) -> np.ndarray:
 def gen_rows_f32(spec: Spec, row_start: int, row_count: int) -> np.ndarray:
     """Rows [row_start, row_start+row_count) of the flat [batch*n*heads, d] view,
     as fp32 values exactly equal to what the device holds (bf16 widened exactly)."""
+    return gen_rows_f32_at(spec, np.arange(row_start, row_start + row_count, dtype=np.int64))
+
+
+def gen_rows_f32_at(spec: Spec, rows) -> np.ndarray:
+    """Arbitrary rows (flat [batch*n*heads] indices) as fp32 values, shape [len(rows), d]."""
     d = spec.d
-    rows = np.arange(row_start, row_start + row_count, dtype=np.int64)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    row_count = len(rows)
     cols = np.arange(d, dtype=np.int64)
     idx = rows[:, None] * d + cols[None, :]
     z = raw_normal(spec.seed, spec.tensor_id, idx)

@@ -71,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError("nvcc failed")
     if force or jobs or not os.path.exists(LIB):
-        cmd = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB, "-ldl"]
+        cmd = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB, "-ldl", "-Xlinker", "--no-undefined"]
         subprocess.run(cmd, check=True)
     return LIB
 

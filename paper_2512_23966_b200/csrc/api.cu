@@ -109,8 +109,8 @@ loza_status_t choose_path(const loza_attn_args_t* a, const AttnProblem& p, Path*
     if (((int64_t)a->heads * a->n_q) % 128 != 0 && a->heads % 64 != 0)
       return fail(LOZA_ERR_UNSUPPORTED, "bf16 prefill needs H %% 64 == 0 or n_q*H %% 128 == 0");
   } else {
-    if (a->heads != 64 && a->heads != 128)
-      return fail(LOZA_ERR_UNSUPPORTED, "bf16 decode supports H in {64, 128}");
+    if (a->heads != 64) return fail(LOZA_ERR_UNSUPPORTED, "bf16 decode supports H == 64");
+    if (a->batch > 1024) return fail(LOZA_ERR_UNSUPPORTED, "bf16 decode supports batch <= 1024");
   }
   *path = Path::kTc;
   return LOZA_OK;

@@ -23,7 +23,6 @@
 //    normalisation uses the same stale max).
 //  * Persistent: grid = min(#units, SMs/2) clusters, units in reverse order
 //    (heaviest causal rows first).
-#include <cudaTypedefs.h>
 #include <math.h>
 #include <string.h>
 
@@ -304,6 +303,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     const uint32_t sfree0 = mapa(bar(kBarSFree), 0), pfull0 = mapa(bar(kBarPFull), 0), ofree = mapa(bar(kBarOFree), 0);
     const float ln2 = 0.69314718055994531f;
     const int64_t rows_b = (int64_t)p.n_q * p.heads;
+    const float sl2 = p.scale_log2;
+    const int causal = p.causal;
+    const int64_t n_kv = p.n_kv;
     uint32_t g = 0, uc = 0;
     for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
       const Unit U = make_unit(p, unit_index(p, it));
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       for (int i = 0; i < U.n_tiles; ++i) {
         const uint32_t gi = g + i, buf = gi & 1;
         const int64_t k0 = tile_k0(U, i);
-        const bool need_mask = (p.causal && k0 + 127 > U.tok_lo) || (k0 + 128 > p.n_kv);
+        const bool need_mask = (causal && k0 + 127 > U.tok_lo) || (k0 + 128 > n_kv);
         mbar_wait(bar(kBarSFull + buf), (gi >> 1) & 1);
         tc_fence_after();
         uint32_t sr[64];
@@ -333,10 +335,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         const int64_t kbase = k0 + 64 * kh;
 #pragma unroll
         for (int j = 0; j < 64; ++j) {
-          float v = __uint_as_float(sr[j]) * p.scale_log2;
+          float v = __uint_as_float(sr[j]) * sl2;
           if (need_mask) {
             const int64_t kp = kbase + j;
-            if ((p.causal && kp > my_tok) || kp >= p.n_kv) v = -INFINITY;
+            if ((causal && kp > my_tok) || kp >= n_kv) v = -INFINITY;
           }
           x[j] = v;
           tmax = fmaxf(tmax, v);
@@ -440,35 +442,6 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }();
-  return fn;
-}
-
-// 3-D bf16 map {d (contiguous), rows, batch}, box {64, box_rows, 1}, 128B swizzle
-bool encode_3d(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t batch, int64_t row_stride_el,
-               int64_t batch_stride_el, uint32_t box_rows) {
-  auto enc = get_encode();
-  if (!enc) return false;
-  if (rows == 0) rows = 1;
-  if (batch == 0) batch = 1;
-  cuuint64_t dims[3] = {d, rows, batch};
-  cuuint64_t strides[2] = {(cuuint64_t)row_stride_el * 2, (cuuint64_t)(batch_stride_el > 0 ? batch_stride_el : rows * row_stride_el) * 2};
-  cuuint32_t box[3] = {64, box_rows, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 }  // namespace
 
 cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
@@ -516,7 +489,5 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_decode_tc(const AttnProblem&, void*, size_t, cudaStream_t) { return cudaErrorNotSupported; }
-size_t decode_tc_ws_bytes(const AttnProblem&) { return 0; }
 
 }  // namespace loza

@@ -173,12 +173,21 @@ def ssa_prefill(q, k, v=None, pattern=PAPER_PATTERN, scale=None, *, d_v=512, out
     return o
 
 
+_decode_ws_cache = {}
+
+
 def _decode_ws(which, a, pattern, ws):
+    """Decode workspace: split-KV partials + per-sequence counters. The counters must start at zero and the
+    kernel leaves them at zero, so a zero-filled buffer is allocated once per device and reused."""
     need = lib().loza_workspace_size(which, ctypes.byref(a), _pattern(pattern), 1)
     if need == 0:
         return None, 0
     if ws is None or ws.numel() < need:
-        ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+        dev = torch.cuda.current_device()
+        ws = _decode_ws_cache.get(dev)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+            _decode_ws_cache[dev] = ws
     return ws, need
 
 
