@@ -51,6 +51,8 @@ size_t blend_ws_bytes();
 cudaError_t launch_prefill_tc(const AttnProblem& p, cudaStream_t st);
 cudaError_t launch_decode_tc(const AttnProblem& p, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t decode_tc_ws_bytes(const AttnProblem& p);
+bool decode_pair_eligible(const AttnProblem& a, int sms);
+cudaError_t launch_decode_pair(const AttnProblem& a, cudaStream_t st);
 
 void count_launch(uint64_t n = 1);
 loza_status_t fail(loza_status_t st, const char* fmt, ...);
