@@ -143,3 +143,22 @@ def test_ssa_prefill_32k_sampled():
     rng = np.random.default_rng(0)
     toks = sorted(set([0, 127, 128, 1023, 1024, n - 1] + rng.integers(0, n, 10).tolist()))
     _check_rows(o, None, qs, ks, toks, pat, True)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_seqpar_local_emulation_bf16_mla_bitwise(world):
+    """Sequence-parallel prefill (segmented KV [sink | halo | shard] through the tcgen05 kernel) equals the
+    single-GPU prefill bitwise; the exchange is emulated with device copies (virtual ranks)."""
+    pat = (1, 7, 128)
+    n_local = 1024
+    n = n_local * world
+    qs, ks = _specs(7, 1, n, 64)
+    q, kv = empty_filled(qs), empty_filled(ks)
+    ref = loza.ssa_prefill(q, kv, pattern=pat, scale=SCALE)
+    shards = [kv[:, r * n_local:(r + 1) * n_local].contiguous() for r in range(world)]
+    for r in range(world):
+        o = loza.ssa_seqpar_prefill_local(q[:, r * n_local:(r + 1) * n_local].contiguous(), shards[r], None, pat, SCALE,
+                                          rank=r, world=world, rank0_k=shards[0],
+                                          prev_k=shards[r - 1] if r > 0 else None)
+        torch.cuda.synchronize()
+        assert torch.equal(o, ref[:, r * n_local:(r + 1) * n_local]), r
