@@ -16,12 +16,21 @@
 //    registers (a row's 256 logits live in TMEM lanes r and r+64: one max exchange);
 //    P (bf16) to SMEM; O += P V: 32 UMMAs M128 N256 K16 (B = V, MN-major) into the
 //    64x512 fp32 accumulator (256 TMEM columns). TMEM: O 256 + S 2 x 128 = 512 cols.
-//  * Loads: TMA (SWIZZLE_128B). Two rings fed by two producer warps so K and V never
-//    wait on each other: K ring 3 x 16 KB (one 128-key x 64-dim chunk per slot),
-//    V ring 4 x 16 KB (64 keys x 128 dims; one commit per 4 UMMAs: a commit costs ~40 issue cycles). Both CTAs' loads complete on the leader's
-//    barriers; one elected thread of the leader issues every UMMA; commits are
-//    multicast to both CTAs. Q is loaded per chunk so the next unit's first S can
-//    start as soon as the previous unit's last S has consumed that chunk.
+//  * Loads: TMA (SWIZZLE_128B) into ONE ring of 3 x 32 KB slots consumed in UMMA order
+//    (K(0), K(1), V(0), K(2), V(1), ..., V(T-1) per unit): a K item is 128 keys x 2 dim chunks
+//    (4-D box), a V item one 128-key sub-block x 128 dims (4-D box); the RoPE chunk 8 of K has
+//    a one-slot ring of its own. 32 KB items halve the per-item cost on the MMA warp (a wait on a
+//    full barrier ~64 issue cycles, a commit ~40 tensor-pipe cycles; tools/umma_interf.cu) versus
+//    16 KB items. Warp 0 issues the Q and K items, warp 10 the V items of the same sequence, with
+//    a position handshake so mbarrier parities cannot alias (see acquire()). A lean issue loop
+//    reaches ~100 B/clk/SM from L2 (tools/tma_box.cu); the fill rate is bound by bytes in flight,
+//    i.e. by the ring size (SMEM: Q 72 KB + P 32 KB + ring 96 + 16 KB). Both CTAs' loads complete
+//    on the leader's barriers; one elected thread of the leader issues every UMMA; commits are
+//    multicast to both CTAs. Q is loaded per chunk so the next unit's first S can start as soon
+//    as the previous unit's last S has consumed that chunk.
+//  * Epilogue: O -> registers (then O is released to the next unit's PV), bf16, staged in the
+//    P buffer as [64 x 64] swizzled boxes, TMA tensor stores (st.global from 256 threads stalled
+//    the MMA warp's barrier traffic at every unit boundary: +12% end to end when removed).
 //  * FA-style order S(0), S(1), PV(0), S(2), PV(1), ...: the softmax of tile t
 //    overlaps PV(t-1) and S(t+1). Lazy rescaling: O and l are rescaled only when a
 //    row max grows by more than 2^8 (exact; the final normalisation uses the same max).
@@ -37,27 +46,32 @@ namespace loza {
 namespace {
 using namespace sm100;
 
+#define FULL_L(slot) (full_l + 8 * (slot))
+#define QFULL_L(c) (qfull_l + 8 * (c))
 constexpr int kDqk = 576, kDv = 512, kChunks = 9;
 constexpr int kThreads = 352;  // warp 0 Q/K TMA, warp 1 MMA, warps 2-9 softmax/epilogue, warp 10 V TMA
 constexpr int kVWarp = 10;
-constexpr int kKSlots = 3;
-constexpr int kKSlotBytes = 16384;  // 128 keys x 64 dims
-constexpr int kVKeys = 64;                 // keys per V slab
-constexpr int kVSlots = 4;
-constexpr int kVSlotBytes = kVKeys * 256;  // kVKeys keys x 128 dims (two 64-dim column blocks)
-constexpr int kVGroups = 256 / kVKeys;     // slabs per 256-key tile and N-half
+constexpr int kSlots = 3;
+constexpr int kSlotBytes = 32768;
+constexpr int kChunkBytes = 16384;         // 128 keys x 64 dims
+constexpr int kKItems = 4;                 // big-ring K items per tile: chunks {0,1} {2,3} {4,5} {6,7};
+                                           // chunk 8 (RoPE) goes through its own one-slot ring
+constexpr int kVKeys = 128;                // V item: one 128-key sub-block x 128 dims (two 64-dim chunks)
+constexpr int kVGroups = 256 / kVKeys;     // V items per tile and N-half
+constexpr int kVItems = 2 * kVGroups;      // V items per tile
+static_assert(kVKeys * 256 == kSlotBytes, "one slot size");
 constexpr int kQBytes = kChunks * 64 * 128;  // 73728 per CTA
 constexpr int kPBytes = 4 * 64 * 128;        // 32768: 4 key chunks (64 keys) x 64 rows
 constexpr int kOffQ = 0;
 constexpr int kOffP = kOffQ + kQBytes;
-constexpr int kOffK = kOffP + kPBytes;
-constexpr int kOffV = kOffK + kKSlots * kKSlotBytes;
-constexpr int kOffBar = kOffV + kVSlots * kVSlotBytes;  // 229376
-constexpr int kBarKFull = 0;
-constexpr int kBarKEmpty = kBarKFull + kKSlots;
-constexpr int kBarVFull = kBarKEmpty + kKSlots;
-constexpr int kBarVEmpty = kBarVFull + kVSlots;
-constexpr int kBarQFull = kBarVEmpty + kVSlots;  // [9] per Q chunk
+constexpr int kOffRing = kOffP + kPBytes;
+constexpr int kOffRope = kOffRing + kSlots * kSlotBytes;  // 204800: K chunk 8 of the next S
+constexpr int kOffBar = kOffRope + kChunkBytes;            // 221184
+constexpr int kBarFull = 0;
+constexpr int kBarEmpty = kBarFull + kSlots;
+constexpr int kBarRopeFull = kBarEmpty + kSlots;
+constexpr int kBarRopeEmpty = kBarRopeFull + 1;
+constexpr int kBarQFull = kBarRopeEmpty + 1;  // [9] per Q chunk
 constexpr int kBarQEmpty = kBarQFull + kChunks;  // [9]
 constexpr int kBarSFull = kBarQEmpty + kChunks;  // [2]
 constexpr int kBarSFree = kBarSFull + 2;         // [2]
@@ -66,7 +80,8 @@ constexpr int kBarOFull = kBarPFull + 1;         // [2]
 constexpr int kBarOFree = kBarOFull + 2;
 constexpr int kNumBars = kBarOFree + 1;
 constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
-constexpr int kOffRed = (kOffTmemPtr + 4 + 15) & ~15;  // float [2 buf][4 quarter-rows][64]; epilogue reuses it
+constexpr int kOffPub = kOffTmemPtr + 4;                // uint32 [2]: producers' next ring positions
+constexpr int kOffRed = (kOffPub + 8 + 15) & ~15;  // float [2 buf][4 quarter-rows][64]; epilogue reuses it
 constexpr int kSmemUsed = kOffRed + 2 * 4 * 64 * 4;
 // The dynamic smem base is 1024-byte aligned (no static smem; checked at run time), so no slack.
 constexpr int kSmemAlloc = kSmemUsed;
@@ -79,8 +94,10 @@ constexpr uint32_t kArrivalsPerPair = 2 * kSoftmaxWarps;
 
 struct PrefillParams {
   CUtensorMap q_map;
-  CUtensorMap k_map[3];
-  CUtensorMap v_map[3];
+  CUtensorMap k_map[3];   // 3-D, box 128 rows x 1 chunk (the RoPE chunk 8)
+  CUtensorMap k2_map[3];  // 4-D, box 128 rows x 2 chunks
+  CUtensorMap v_map[3];   // 4-D, box 128 rows x 2 chunks
+  CUtensorMap o_map;      // bf16 output, box 64 rows x 64 dims (TMA-store epilogue)
   int64_t seg_begin[3];
   int32_t seg_len[3];
   int32_t nseg;
@@ -93,6 +110,7 @@ struct PrefillParams {
   int32_t out_bf16;
   float* lse;
   int64_t units_per_batch, total_units;
+  int32_t small;              // all index math fits in uint32 (make_unit fast path)
   unsigned long long* trace;  // debug timeline (cluster 0, leader CTA), NULL in production
 };
 
@@ -103,35 +121,45 @@ struct Unit {
   int32_t n_sink, loc_begin, n128, n_tiles;  // 128-key sub-blocks; 256-key S tiles
 };
 
-__device__ __forceinline__ Unit make_unit(const PrefillParams& p, int64_t u) {
+// Index math in T: uint32_t when every quantity fits (PrefillParams::small, the common case) -- the
+// 64-bit divisions of the general path cost ~1.4K cycles per unit on the MMA warp's critical path.
+template <typename T>
+__device__ __forceinline__ Unit make_unit_t(const PrefillParams& p, int64_t u64) {
   Unit U;
-  U.bi = (int32_t)(u / p.units_per_batch);
-  U.row0 = (u % p.units_per_batch) * 128;
-  const int64_t rows = (int64_t)p.n_q * p.heads;
-  int64_t rlast = U.row0 + 127;
+  const T u = (T)u64, upb = (T)p.units_per_batch, heads = (T)p.heads;
+  const T bi = u / upb;
+  const T row0 = (u - bi * upb) * 128;
+  const T rows = (T)p.n_q * heads;
+  T rlast = row0 + 127;
   if (rlast > rows - 1) rlast = rows - 1;
-  U.tok_lo = p.q_start + U.row0 / p.heads;
-  U.tok_hi = p.q_start + rlast / p.heads;
-  const int64_t last_sub = p.causal ? U.tok_hi / 128 : (p.n_kv - 1) / 128;
+  U.bi = (int32_t)bi;
+  U.row0 = (int64_t)row0;
+  const T tok_lo = (T)p.q_start + row0 / heads, tok_hi = (T)p.q_start + rlast / heads;
+  U.tok_lo = (int64_t)tok_lo;
+  U.tok_hi = (int64_t)tok_hi;
+  const T last_sub = p.causal ? tok_hi / 128 : ((T)p.n_kv - 1) / 128;
   if (!p.sparse) {
     U.n_sink = 0;
     U.loc_begin = 0;
     U.n128 = (int32_t)(last_sub + 1);
   } else {
-    const int64_t tpb = p.b / 128, QB = U.tok_lo / p.b;
+    const int64_t tpb = p.b / 128, QB = (int64_t)(tok_lo / (T)p.b);
     int64_t sink_end = (QB + 1 < p.s ? QB + 1 : p.s) * tpb;
-    if (sink_end > last_sub + 1) sink_end = last_sub + 1;
+    if (sink_end > (int64_t)last_sub + 1) sink_end = (int64_t)last_sub + 1;
     int64_t lb = QB - p.l + 1;
     if (lb < p.s) lb = p.s;
     lb *= tpb;
     int64_t le = (QB + 1) * tpb;
-    if (le > last_sub + 1) le = last_sub + 1;
+    if (le > (int64_t)last_sub + 1) le = (int64_t)last_sub + 1;
     U.n_sink = (int32_t)sink_end;
     U.loc_begin = (int32_t)lb;
     U.n128 = (int32_t)(sink_end + (le > lb ? le - lb : 0));
   }
   U.n_tiles = (U.n128 + 1) / 2;
   return U;
+}
+__device__ __forceinline__ Unit make_unit(const PrefillParams& p, int64_t u) {
+  return p.small ? make_unit_t<uint32_t>(p, u) : make_unit_t<int64_t>(p, u);
 }
 // start key of the j-th selected 128-key sub-block, or -1 if j is past the list
 __device__ __forceinline__ int64_t sub_k0(const Unit& U, int j) {
@@ -177,14 +205,12 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   float* red = reinterpret_cast<float*>(smem + kOffRed);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kKSlots; ++i) {
-      mbar_init(bar(kBarKFull + i), 1);
-      mbar_init(bar(kBarKEmpty + i), 1);
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(bar(kBarFull + i), 1);
+      mbar_init(bar(kBarEmpty + i), 1);
     }
-    for (int i = 0; i < kVSlots; ++i) {
-      mbar_init(bar(kBarVFull + i), 1);
-      mbar_init(bar(kBarVEmpty + i), 1);
-    }
+    mbar_init(bar(kBarRopeFull), 1);
+    mbar_init(bar(kBarRopeEmpty), 1);
     for (int i = 0; i < kChunks; ++i) {
       mbar_init(bar(kBarQFull + i), 1);
       mbar_init(bar(kBarQEmpty + i), 1);
@@ -196,12 +222,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     }
     mbar_init(bar(kBarPFull), kArrivalsPerPair);
     mbar_init(bar(kBarOFree), kArrivalsPerPair);
+    reinterpret_cast<volatile uint32_t*>(smem + kOffPub)[0] = 0;
+    reinterpret_cast<volatile uint32_t*>(smem + kOffPub)[1] = 0;
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.q_map);
     for (int i = 0; i < p.nseg; ++i) {
       prefetch_tmap(&p.k_map[i]);
+      prefetch_tmap(&p.k2_map[i]);
       prefetch_tmap(&p.v_map[i]);
     }
   }
@@ -219,10 +248,67 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   // descriptors / coordinates in uniform registers); one elected lane issues each TMA / UMMA.
   // A lane-0-guarded issue loop made ptxas emit an R2UR "uniformisation loop" per UMMA,
   // which capped the issue rate at ~40% of the tensor pipe (tools/umma_interf.cu).
+  // Ring position -> (slot, phase), advanced incrementally (no divisions on the issue path).
+  struct RingPos {
+    uint32_t slot = 0, phase = 0, pos = 0;
+    __device__ __forceinline__ void step() {
+      ++pos;
+      if (++slot == kSlots) {
+        slot = 0;
+        phase ^= 1;
+      }
+    }
+    __device__ __forceinline__ void skip(int n) {
+      for (int i = 0; i < n; ++i) step();
+    }
+  };
+  // Two producers share the ring. A parity wait on empty[slot] for use j is only sound once use j-1 of
+  // that slot has passed its own wait (else the barrier may be two phases behind and the parity aliases).
+  // When use j-1 belongs to the other producer this is not implied by program order, so each producer
+  // publishes the ring position of its next item (all its items before it are issued) and waits until
+  // the other's published position passes pos - kSlots. No deadlock: everything before the other's
+  // published position is issued, so it can always advance.
+  volatile uint32_t* pub = reinterpret_cast<volatile uint32_t*>(smem + kOffPub);
+  auto acquire = [&](const RingPos& rp, int me) {
+    if (lane == 0) pub[me] = rp.pos;
+    if (rp.pos >= (uint32_t)kSlots)
+      while (pub[me ^ 1] <= rp.pos - kSlots) {
+      }
+    __syncwarp();
+    mbar_wait(bar(kBarEmpty + rp.slot), rp.phase ^ 1);
+  };
   if (warp == 0) {
-    // ===================================================== Q + K TMA producer (both CTAs)
+    // ===================================================== Q + K items producer (both CTAs)
     const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
-    uint32_t uc = 0, kc = 0;
+    const uint32_t full_l = mapa(bar(kBarFull), 0), qfull_l = mapa(bar(kBarQFull), 0),
+                   rope_l = mapa(bar(kBarRopeFull), 0);
+    const uint32_t ring = sbase + kOffRing;
+    RingPos rp;
+    uint32_t uc = 0;
+    uint32_t gk = 0;
+    auto load_k = [&](const Unit& U, int i) {
+      int sg;
+      int32_t row;
+      kv_coord(p, sub_k0(U, 2 * i + (int)rank), 0, sg, row);  // CTA r stages sub-block 2i+r
+      // chunk 8 first: its slot was freed by the previous S, long before this one needs it
+      mbar_wait(bar(kBarRopeEmpty), (gk & 1) ^ 1);
+      if (elect_one()) {
+        if (rank == 0) mbar_arrive_expect_tx(bar(kBarRopeFull), 2 * kChunkBytes);
+        tma_load_3d_pair(sbase + kOffRope, &p.k_map[sg], 8 * 64, row, U.bi, rope_l, pol_kv);
+      }
+      __syncwarp();
+      for (int j = 0; j < kKItems; ++j, rp.step()) {
+        acquire(rp, 0);
+        if (j == 0) TRACE(13, gk);
+        if (j == kKItems - 1) TRACE(14, gk);
+        if (elect_one()) {
+          if (rank == 0) mbar_arrive_expect_tx(bar(kBarFull + rp.slot), 2 * kSlotBytes);
+          tma_load_4d_pair(ring + rp.slot * kSlotBytes, &p.k2_map[sg], 0, row, 2 * j, U.bi, FULL_L(rp.slot), pol_kv);
+        }
+        __syncwarp();
+      }
+      ++gk;
+    };
     for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
       const Unit U = make_unit(p, unit_index(p, it));
       for (int c = 0; c < kChunks; ++c) {
@@ -230,62 +316,67 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         if (elect_one()) {
           if (rank == 0) mbar_arrive_expect_tx(bar(kBarQFull + c), 2 * 8192);
           tma_load_3d_pair(sbase + kOffQ + c * 8192, &p.q_map, c * 64, (int32_t)(U.row0 + 64 * rank), U.bi,
-                           mapa(bar(kBarQFull + c), 0), pol_q);
+                           QFULL_L(c), pol_q);
         }
         __syncwarp();
       }
-      for (int i = 0; i < U.n_tiles; ++i) {
+      load_k(U, 0);
+      for (int i = 1; i < U.n_tiles; ++i) {
+        load_k(U, i);
+        rp.skip(kVItems);  // V(i-1): warp kVWarp
+      }
+      rp.skip(kVItems);
+    }
+    if (lane == 0) pub[0] = 0xFFFFFFFFu;
+  } else if (warp == kVWarp) {
+    // ===================================================== V items producer (both CTAs)
+    const uint64_t pol_kv = policy_evict_last();
+    const uint32_t full_l = mapa(bar(kBarFull), 0);
+    const uint32_t ring = sbase + kOffRing;
+    RingPos rp;
+    uint32_t gv = 0;
+    auto load_v = [&](const Unit& U, int i) {
+      for (int kg = 0; kg < kVGroups; ++kg) {  // sub-block A then B of tile i
         int sg;
         int32_t row;
-        kv_coord(p, sub_k0(U, 2 * i + (int)rank), 0, sg, row);  // CTA r stages sub-block 2i+r
-        for (int c = 0; c < kChunks; ++c, ++kc) {
-          const uint32_t slot = kc % kKSlots;
-          mbar_wait(bar(kBarKEmpty + slot), ((kc / kKSlots) & 1) ^ 1);
+        kv_coord(p, sub_k0(U, 2 * i + kg), 0, sg, row);
+        for (int nh = 0; nh < 2; ++nh, rp.step()) {
+          acquire(rp, 1);
+          if (kg == 0 && nh == 0) TRACE(15, gv);
+          if (kg == 1 && nh == 1) TRACE(16, gv);
           if (elect_one()) {
-            if (rank == 0) mbar_arrive_expect_tx(bar(kBarKFull + slot), 2 * kKSlotBytes);
-            tma_load_3d_pair(sbase + kOffK + slot * kKSlotBytes, &p.k_map[sg], c * 64, row, U.bi,
-                             mapa(bar(kBarKFull + slot), 0), pol_kv);
+            if (rank == 0) mbar_arrive_expect_tx(bar(kBarFull + rp.slot), 2 * kSlotBytes);
+            // dims [256 nh + 128 r, +128) = column chunks 4 nh + 2 r, +1 (one 4-D box)
+            tma_load_4d_pair(ring + rp.slot * kSlotBytes, &p.v_map[sg], 0, row, 4 * nh + 2 * (int)rank, U.bi,
+                             FULL_L(rp.slot), pol_kv);
           }
           __syncwarp();
         }
       }
-    }
-  } else if (warp == kVWarp) {
-    // ===================================================== V TMA producer (both CTAs)
-    const uint64_t pol_kv = policy_evict_last();
-    uint32_t vc = 0;
+      ++gv;
+    };
     for (int64_t it = cid; it < n_iter_total; it += ncl) {
       const Unit U = make_unit(p, unit_index(p, it));
-      for (int i = 0; i < U.n_tiles; ++i) {
-        for (int kg = 0; kg < kVGroups; ++kg) {  // kVKeys-key groups: first half sub-block A, second half B
-          int sg;
-          int32_t row;
-          kv_coord(p, sub_k0(U, 2 * i + kg / (kVGroups / 2)), kVKeys * (kg % (kVGroups / 2)), sg, row);
-          for (int nh = 0; nh < 2; ++nh, ++vc) {
-            const uint32_t slot = vc % kVSlots;
-            mbar_wait(bar(kBarVEmpty + slot), ((vc / kVSlots) & 1) ^ 1);
-            if (elect_one()) {
-              if (rank == 0) mbar_arrive_expect_tx(bar(kBarVFull + slot), 2 * kVSlotBytes);
-              const uint32_t fb = mapa(bar(kBarVFull + slot), 0);
-              for (int e = 0; e < 2; ++e)
-                tma_load_3d_pair(sbase + kOffV + slot * kVSlotBytes + e * (kVKeys * 128), &p.v_map[sg],
-                                 256 * nh + 128 * (int)rank + 64 * e, row, U.bi, fb, pol_kv);
-            }
-            __syncwarp();
-          }
-        }
+      rp.skip(kKItems);  // K(0)
+      for (int i = 1; i < U.n_tiles; ++i) {
+        rp.skip(kKItems);  // K(i)
+        load_v(U, i - 1);
       }
+      load_v(U, U.n_tiles - 1);
     }
+    if (lane == 0) pub[1] = 0xFFFFFFFFu;
   } else if (warp == 1) {
     // ===================================================== MMA issuer (leader CTA only)
     if (rank == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(128, 256, false, false);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 256, false, true);
       const uint64_t dq = sdesc_sw128(sbase + kOffQ, 16, 1024);  // Q chunk c, K step k: + (8192c + 32k) >> 4
-      const uint64_t dk = sdesc_sw128(sbase + kOffK, 16, 1024);  // K slot j: + 16384 j >> 4
+      const uint64_t dk = sdesc_sw128(sbase + kOffRing, 16, 1024);  // ring slot j, chunk cc: + (32768 j + 16384 cc) >> 4
       const uint64_t dp = sdesc_sw128(sbase + kOffP, 16, 1024);  // P chunk: + 8192 chunk >> 4
-      const uint64_t dv = sdesc_sw128(sbase + kOffV, kVKeys * 128, 1024);  // V slot j (MN-major)
-      uint32_t uc = 0, g = 0, kc = 0, vc = 0;
+      const uint64_t dv = sdesc_sw128(sbase + kOffRing, kVKeys * 128, 1024);  // ring slot j as a V item (MN-major,
+                                                                              // 64-dim chunks kVKeys*128 B apart)
+      uint32_t uc = 0, g = 0;
+      RingPos rp;
       long long kwait = 0, vwait = 0;
       auto issue_s = [&](uint32_t gi, bool first, bool last) {
         const uint32_t buf = gi & 1;
@@ -295,22 +386,38 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         TRACE(1, gi);
         tc_fence_after();
         const uint32_t d = tmem + kTmemS + 128 * buf;
-        for (int c = 0; c < kChunks; ++c, ++kc) {
-          const uint32_t slot = kc % kKSlots;
+        for (int j = 0; j <= kKItems; ++j) {  // big items j < 4 (chunks 2j, 2j+1), then the RoPE chunk
+          const bool rope = j == kKItems;
+          const uint32_t slot = rp.slot;
+          const int nc = rope ? 1 : 2;
           const long long w0 = clock64();
-          if (first) mbar_wait(bar(kBarQFull + c), uc & 1);
-          mbar_wait(bar(kBarKFull + slot), (kc / kKSlots) & 1);
+          if (first) {
+            mbar_wait(bar(kBarQFull + 2 * j), uc & 1);
+            if (nc == 2) mbar_wait(bar(kBarQFull + 2 * j + 1), uc & 1);
+          }
+          if (rope)
+            mbar_wait(bar(kBarRopeFull), gi & 1);
+          else
+            mbar_wait(bar(kBarFull + slot), rp.phase);
           kwait += clock64() - w0;
           tc_fence_after();
+          const uint32_t kaddr = rope ? (uint32_t)(kOffRope - kOffRing) : kSlotBytes * slot;
           if (elect_one()) {
+            for (int cc = 0; cc < nc; ++cc) {
+              const int c = 2 * j + cc;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              umma_bf16_pair(d, dq + (uint64_t)((8192 * c + 32 * k) >> 4),
-                             dk + (uint64_t)((kKSlotBytes * slot + 32 * k) >> 4), idesc_s, (c | k) != 0);
-            umma_commit_pair_mc(bar(kBarKEmpty + slot), 3);
-            if (last) umma_commit_pair_mc(bar(kBarQEmpty + c), 3);
+              for (int k = 0; k < 4; ++k)
+                umma_bf16_pair(d, dq + (uint64_t)((8192 * c + 32 * k) >> 4),
+                               dk + (uint64_t)((kaddr + kChunkBytes * cc + 32 * k) >> 4), idesc_s, (c | k) != 0);
+            }
+            umma_commit_pair_mc(bar(rope ? kBarRopeEmpty : kBarEmpty + slot), 3);
+            if (last) {
+              umma_commit_pair_mc(bar(kBarQEmpty + 2 * j), 3);
+              if (nc == 2) umma_commit_pair_mc(bar(kBarQEmpty + 2 * j + 1), 3);
+            }
           }
           __syncwarp();
+          if (!rope) rp.step();
         }
         if (elect_one()) umma_commit_pair_mc(bar(kBarSFull + buf), 3);
         __syncwarp();
@@ -325,10 +432,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         TRACE(4, gi);
         tc_fence_after();
         for (int kg = 0; kg < kVGroups; ++kg)
-          for (int nh = 0; nh < 2; ++nh, ++vc) {
-            const uint32_t slot = vc % kVSlots;
+          for (int nh = 0; nh < 2; ++nh, rp.step()) {
+            const uint32_t slot = rp.slot;
             const long long w0 = clock64();
-            mbar_wait(bar(kBarVFull + slot), (vc / kVSlots) & 1);
+            mbar_wait(bar(kBarFull + slot), rp.phase);
             vwait += clock64() - w0;
             tc_fence_after();
             if (elect_one()) {
@@ -336,10 +443,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
               for (int kk = 0; kk < kVKeys / 16; ++kk) {
                 const int key = kg * kVKeys + 16 * kk;  // key of the 256-key tile (P column)
                 umma_bf16_pair(tmem + kTmemO + 128 * nh, dp + (uint64_t)((8192 * (key >> 6) + 2 * (key & 63)) >> 4),
-                               dv + (uint64_t)((kVSlotBytes * slot + 2048 * kk) >> 4), idesc_pv,
+                               dv + (uint64_t)((kSlotBytes * slot + 2048 * kk) >> 4), idesc_pv,
                                !(first && kg == 0 && kk == 0));
               }
-              umma_commit_pair_mc(bar(kBarVEmpty + slot), 3);
+              umma_commit_pair_mc(bar(kBarEmpty + slot), 3);
             }
             __syncwarp();
           }
@@ -490,24 +597,58 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       const float ltot = (ls[r] + ls[64 + r]) + (ls[128 + r] + ls[192 + r]);
       const float inv = 1.0f / ltot;
       named_bar_sync(1, kSmThreads);  // everyone has read ls before the next unit's first exchange writes red
-      char* obase = reinterpret_cast<char*>(p.o) +
-                    ((int64_t)U.bi * p.o_sb + (row_ok ? row_g : 0) * kDv) * (p.out_bf16 ? 2 : 4);
+      if (p.out_bf16) {
+        // O (this thread: row r, dims 256 ch + 128 kh + [0, 128)) -> bf16 registers; O is then free for
+        // the next unit's PV. Stores go out as TMA boxes [64 rows x 64 dims] staged in the P buffer (idle
+        // between PV(T-1) and the next unit's first softmax): a flood of st.global from 256 threads queues
+        // ahead of the MMA warp's mbarrier operations and stalls the tensor pipe at every unit boundary.
+        uint32_t w[64];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t ov[32];
+          tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            w[16 * c + j] = pack_bf16x2(__uint_as_float(ov[2 * j]) * inv, __uint_as_float(ov[2 * j + 1]) * inv);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(ofree);
+        const uint32_t stage = sbase + kOffP;
+#pragma unroll
+        for (int rd = 0; rd < 2; ++rd) {  // round rd: the warps with ch == rd, dims [256 rd, +256) = 4 boxes
+          if (ch == (uint32_t)rd) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t box = stage + (2 * kh + (c >> 1)) * 8192 + r * 128;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t u = (c & 1) * 4 + q;
+                st_shared_v4(box + ((u ^ (r & 7)) << 4), w[16 * c + 4 * q], w[16 * c + 4 * q + 1],
+                             w[16 * c + 4 * q + 2], w[16 * c + 4 * q + 3]);
+              }
+            }
+            fence_proxy_async_smem();
+          }
+          named_bar_sync(1, kSmThreads);
+          if (warp == 2 && lane == 0) {
+            for (int m = 0; m < 4; ++m)
+              tma_store_3d(&p.o_map, stage + m * 8192, 64 * (4 * rd + m), (int32_t)(U.row0 + 64 * rank), U.bi);
+            bulk_commit_group();
+            bulk_wait_group_read0();  // staging may be overwritten
+          }
+          named_bar_sync(1, kSmThreads);
+        }
+      } else {
+        char* obase = reinterpret_cast<char*>(p.o) + ((int64_t)U.bi * p.o_sb + (row_ok ? row_g : 0) * kDv) * 4;
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t ov[32];
-        tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ov);
-        tmem_wait_ld();
-        const int dim0 = 256 * (int)ch + 128 * (int)kh + 32 * c;
-        if (row_ok) {
-          if (p.out_bf16) {
-            uint32_t w[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              w[j] = pack_bf16x2(__uint_as_float(ov[2 * j]) * inv, __uint_as_float(ov[2 * j + 1]) * inv);
-            char* dst = obase + dim0 * 2;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) st_global_v4(dst + 16 * q, w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-          } else {
+        for (int c = 0; c < 4; ++c) {
+          uint32_t ov[32];
+          tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ov);
+          tmem_wait_ld();
+          const int dim0 = 256 * (int)ch + 128 * (int)kh + 32 * c;
+          if (row_ok) {
             char* dst = obase + dim0 * 4;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
@@ -517,16 +658,17 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                            __float_as_uint(__uint_as_float(ov[4 * q + 3]) * inv));
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(ofree);
       }
       if (p.lse && row_ok && q4 == 0) {
         const int64_t h = row_g % p.heads, tl_ = row_g / p.heads;
         p.lse[((int64_t)U.bi * p.heads + h) * p.n_q + tl_] = (m_used + __log2f(ltot)) * ln2;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(ofree);
       g += U.n_tiles;
     }
+    if (warp == 2 && lane == 0) bulk_wait_group0();  // output stores complete before exit
   }
   __syncwarp();
   tc_fence_before();
@@ -564,7 +706,10 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
   p.trace = g_debug_trace;
   p.total_units = p.units_per_batch * a.batch;
   if (p.total_units == 0) return cudaSuccess;
+  const int64_t lim = (int64_t)1 << 31;
+  p.small = p.total_units * 128 < lim && rows + 128 < lim && a.q_start + a.n_q + 128 < lim && a.n_kv + 128 < lim;
   if (!encode_3d(&p.q_map, a.q, kDqk, rows, a.batch, kDqk, a.q_sb, 64)) return cudaErrorInvalidValue;
+  if (a.out_bf16 && !encode_3d(&p.o_map, a.o, kDv, rows, a.batch, kDv, a.o_sb, 64)) return cudaErrorInvalidValue;
   p.nseg = a.kv.nseg;
   for (int i = 0; i < a.kv.nseg; ++i) {
     const KvSeg& s = a.kv.seg[i];
@@ -572,7 +717,8 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
     const uint64_t len = (uint64_t)(s.pos_end - s.pos_begin);
     p.seg_len[i] = (int32_t)len;
     if (!encode_3d(&p.k_map[i], s.k, kDqk, len, a.batch, s.k_st, s.k_sb, 128)) return cudaErrorInvalidValue;
-    if (!encode_3d(&p.v_map[i], s.v, kDv, len, a.batch, s.v_st, s.v_sb, kVKeys)) return cudaErrorInvalidValue;
+    if (!encode_4d_chunks(&p.k2_map[i], s.k, kDqk, len, a.batch, s.k_st, s.k_sb, 128, 2)) return cudaErrorInvalidValue;
+    if (!encode_4d_chunks(&p.v_map[i], s.v, kDv, len, a.batch, s.v_st, s.v_sb, kVKeys, 2)) return cudaErrorInvalidValue;
   }
   static bool attr_set = false;
   if (!attr_set) {
@@ -590,5 +736,5 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
 
 }  // namespace loza
 
-// debug hook (not part of include/loza.h): record a clock64 timeline of cluster 0 into dev_ptr[11*64]
+// debug hook (not part of include/loza.h): record a clock64 timeline of cluster 0 into dev_ptr[17*64]
 extern "C" void loza_debug_set_trace(void* dev_ptr) { loza::g_debug_trace = (unsigned long long*)dev_ptr; }

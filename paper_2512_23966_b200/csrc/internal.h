@@ -70,4 +70,6 @@ namespace loza {
 // 3-D bf16 TMA map {d (contiguous), rows, batch}, box {64, box_rows, 1}, SWIZZLE_128B (tma_host.cu)
 bool encode_3d(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t batch, int64_t row_stride_el,
                int64_t batch_stride_el, uint32_t box_rows);
+bool encode_4d_chunks(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t batch,
+                      int64_t row_stride_el, int64_t batch_stride_el, uint32_t box_rows, uint32_t box_chunks);
 }  // namespace loza

@@ -37,5 +37,24 @@ bool encode_3d(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint
   return r == CUDA_SUCCESS;
 }
 
+// 4-D bf16 view {64 (contiguous), rows, d/64 column chunks, batch} of a [batch, rows, d] tensor: one box
+// {64, box_rows, box_chunks, 1} fetches box_chunks adjacent 64-column chunks; in SMEM the chunks follow
+// each other (box_rows x 128 B each), i.e. the layout of box_chunks separate 3-D loads.
+bool encode_4d_chunks(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t batch,
+                      int64_t row_stride_el, int64_t batch_stride_el, uint32_t box_rows, uint32_t box_chunks) {
+  auto enc = get_encode();
+  if (!enc || d % 64 != 0) return false;
+  if (rows == 0) rows = 1;
+  if (batch == 0) batch = 1;
+  cuuint64_t dims[4] = {64, rows, d / 64, batch};
+  cuuint64_t strides[3] = {(cuuint64_t)row_stride_el * 2, 128,
+                           (cuuint64_t)(batch_stride_el > 0 ? batch_stride_el : rows * row_stride_el) * 2};
+  cuuint32_t box[4] = {64, box_rows, box_chunks, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 
 }  // namespace loza

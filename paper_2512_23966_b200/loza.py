@@ -14,7 +14,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libloza.so")
+# LOZA_LIB: development override (A/B builds of the same library, tools/build_variant.py); default in-tree .so
+LIB_PATH = os.environ.get("LOZA_LIB") or os.path.join(_HERE, "libloza.so")
 
 LOZA_F32, LOZA_BF16 = 0, 1
 LOZA_WS_DECODE, LOZA_WS_FULL_DECODE, LOZA_WS_BLEND, LOZA_WS_SEQPAR = 0, 1, 2, 3
