@@ -455,15 +455,19 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         TRACE(5, gi);
         if (p.trace && cid == 0 && gi < 64 && lane == 0) p.trace[12 * 64 + gi] = vwait;
       };
+      // the next unit is decoded before the last PV, whose wait for the last P would otherwise be followed
+      // by ~1K cycles of index math with the tensor pipe idle
+      Unit U = make_unit(p, unit_index(p, cid < n_iter_total ? cid : 0));
       for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
-        const Unit U = make_unit(p, unit_index(p, it));
         const uint32_t g0 = g;
         for (int i = 0; i < U.n_tiles; ++i) {
           issue_s(g0 + i, i == 0, i == U.n_tiles - 1);
           if (i >= 1) issue_pv(g0 + i - 1, i - 1 == 0);
         }
-        issue_pv(g0 + U.n_tiles - 1, U.n_tiles == 1);
-        g += U.n_tiles;
+        const int nt = U.n_tiles;
+        if (it + ncl < n_iter_total) U = make_unit(p, unit_index(p, it + ncl));
+        issue_pv(g0 + nt - 1, nt == 1);
+        g += nt;
       }
     }
   } else {
