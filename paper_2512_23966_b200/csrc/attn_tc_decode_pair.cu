@@ -228,9 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           const uint32_t dst = acquire();
           if (elect_one()) {
             mbar_arrive_expect_tx(bar(kBarRingFull + stage), kStageBytes);
-            for (int e = 0; e < 4; ++e)
-              tma_load_3d(dst + e * 4096, &p.v_map, 256 * nh + 64 * e, k0 + 32 * kq, bi, bar(kBarRingFull + stage),
-                          pol_kv);
+            // one 4-D box: 32 keys x dim chunks 4 nh .. 4 nh + 3 (smem [chunk][32 keys][64 dims])
+            tma_load_4d(dst, &p.v_map, 0, k0 + 32 * kq, 4 * nh, bi, bar(kBarRingFull + stage), pol_kv);
           }
           __syncwarp();
           next();
@@ -263,9 +262,12 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       mbar_wait(bar(kBarSFree + buf), ((gi >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem + kTmemS + 64 * buf;
+      long long kw = 0;
       for (int cc = 0; cc < kChunks; ++cc) {
+        const long long w0 = clock64();
         if (gi == 0) mbar_wait(bar(kBarQFull + cc), 0);
         mbar_wait(bar(kBarRingFull + stage), phase);
+        kw += clock64() - w0;
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -280,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       if (elect_one()) umma_commit_1sm(bar(kBarSFull + buf));
       __syncwarp();
       DTRACE(2, gi);
+      if (p.trace && blockIdx.x == 0 && gi < 32 && lane == 0) p.trace[12 * 32 + 4 * p.batch + gi] = kw;
     };
     auto issue_pv = [&](uint32_t gi, bool first) {
       const uint32_t buf = gi & 1;
@@ -287,9 +290,12 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       mbar_wait(bar(kBarPFull + buf), (gi >> 1) & 1);
       DTRACE(4, gi);
       tc_fence_after();
+      long long vw = 0;
       for (int kq = 0; kq < 4; ++kq)
         for (int nh = 0; nh < 2; ++nh) {
+          const long long w0 = clock64();
           mbar_wait(bar(kBarRingFull + stage), phase);
+          vw += clock64() - w0;
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
@@ -308,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       if (elect_one()) umma_commit_1sm(bar(kBarOFull + buf));
       __syncwarp();
       DTRACE(5, gi);
+      if (p.trace && blockIdx.x == 0 && gi < 32 && lane == 0) p.trace[12 * 32 + 4 * p.batch + 32 + gi] = vw;
     };
     for (int i = 0; i < n; ++i) {
       issue_s((uint32_t)i);
@@ -561,7 +568,8 @@ cudaError_t launch_decode_pair(const AttnProblem& a, cudaStream_t st) {
   const KvSeg& s = a.kv.seg[0];
   if (!encode_3d(&p.q_map, a.q, kDqk, kH, a.batch, a.q_sh, a.q_sb, 64)) return cudaErrorInvalidValue;
   if (!encode_3d(&p.k_map, s.k, kDqk, (uint64_t)a.n_kv, a.batch, s.k_st, s.k_sb, 128)) return cudaErrorInvalidValue;
-  if (!encode_3d(&p.v_map, s.v, kDv, (uint64_t)a.n_kv, a.batch, s.v_st, s.v_sb, 32)) return cudaErrorInvalidValue;
+  if (!encode_4d_chunks(&p.v_map, s.v, kDv, (uint64_t)a.n_kv, a.batch, s.v_st, s.v_sb, 32, 4))
+    return cudaErrorInvalidValue;
   if (a.out_bf16 && !encode_3d(&p.o_map, a.o, kDv, kH, a.batch, a.o_sh, a.o_sb, 64)) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {

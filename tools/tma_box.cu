@@ -7,14 +7,6 @@
 #include "sm100.cuh"
 using namespace loza::sm100;
 
-__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
-                                            int32_t c3, uint32_t bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar), "l"(policy)
-      : "memory");
-}
 
 template <int C, int SLOTS>  // C chunks per instruction; SLOTS instructions in flight
 __global__ void __launch_bounds__(64, 1) bw(const __grid_constant__ CUtensorMap map, int n, int loads,

@@ -9,7 +9,7 @@ B, ctx = 64, 131072
 cache = empty_filled(Spec(seed=0, tensor_id=TID_K, batch=B, n=ctx, heads=1, d=576))
 q = empty_filled(Spec(seed=1, tensor_id=TID_Q, batch=B, n=1, heads=64, d=576))
 seq = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
-tr = torch.zeros(12 * 32 + 2 * 2 * B, dtype=torch.int64, device="cuda")
+tr = torch.zeros(12 * 32 + 2 * 2 * B + 64, dtype=torch.int64, device="cuda")
 L = loza.lib()
 L.loza_debug_set_pair_trace.argtypes = [ctypes.c_void_p]
 for _ in range(3):
@@ -23,7 +23,10 @@ print("event time (us, incl. host launch gap)", s.elapsed_time(e) * 1e3)
 L.loza_debug_set_pair_trace(ctypes.c_void_p(0))
 ta = tr.cpu().numpy().astype("int64")
 t = ta[:12 * 32].reshape(12, 32)
-sp = ta[12 * 32:].reshape(2 * B, 2)
+sp = ta[12 * 32:12 * 32 + 4 * B].reshape(2 * B, 2)
+kw = ta[12 * 32 + 4 * B:12 * 32 + 4 * B + 32]
+vw = ta[12 * 32 + 4 * B + 32:]
+print('ring waits in S per tile', kw[:6], ' in PV', vw[:6])
 base = t[0, 0]
 for nm, row in zip(["setup", "S_start", "S_issued", "PV_start", "PV_pok", "PV_issued", "sm_wait", "sm_sfull", "sm_parr", "piece_end", "merge_sent", "done"], t):
     print(f"{nm:>10s} " + " ".join(f"{(x - base) if x > 0 else -1:7d}" for x in row[:9]))
