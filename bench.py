@@ -329,6 +329,20 @@ def extra_rows(args, q, kv, o, flush, peaks):
                        / peaks["bf16_tflops"],
                        "full_frac_tensor": full_pairs(n8) * FLOP_PER_PAIR / (np.mean(t_full) * 1e-3) / 1e12
                        / peaks["bf16_tflops"]}
+    # fused calibration forward: SSA + Eq. 3 + d_alpha in one kernel (O' never stored)
+    t_fu = _time_events(lambda: loza.ssa_prefill_blend(q8, kv8, of, alpha, dh, pattern=PATTERN, scale=scale, out=oh),
+                        5, 2, flush)
+    t_ff = _time_events(lambda: loza.ssa_prefill_blend(q8, kv8, of, alpha, pattern=PATTERN, scale=scale, out=oh),
+                        5, 2, flush)
+    t_bf = _time_events(lambda: loza.loza_blend(of, osp, alpha, out=oh), 10, 3, flush)
+    fu_ms = float(np.mean(t_fu))
+    out["calibration_fused_8k"] = {
+        "fused_ms": fu_ms, "unfused_ms": float(np.mean(t_ssa)) + float(np.mean(t_bl)),
+        "speedup_vs_unfused": (float(np.mean(t_ssa)) + float(np.mean(t_bl))) / fu_ms,
+        "fused_fwd_only_ms": float(np.mean(t_ff)), "unfused_fwd_only_ms": float(np.mean(t_ssa)) + float(np.mean(t_bf)),
+        "ssa_frac_tensor_in_fused": ssa_pairs(n8, *PATTERN) * FLOP_PER_PAIR / (fu_ms * 1e-3) / 1e12
+        / peaks["bf16_tflops"],
+        "note": "unfused = ssa_prefill (writes O') + loza_blend with d_alpha (reads O, O', dO_hat; writes O_hat)"}
     del of, osp, dh, oh
     # decode B64 at 128K / 512K / 1M (configs[3])
     if not args.no_decode:

@@ -121,6 +121,22 @@ loza_status_t loza_blend(const void* o_full, const void* o_sparse, const float* 
                          const void* d_o_hat, double* d_alpha_dev, int64_t numel, loza_dtype_t dtype,
                          int32_t* status_dev, void* ws, size_t ws_bytes, loza_stream_t stream);
 
+/* Fused calibration forward (Eq. 3, with O' = the SSA prefill of
+ * `args`, Eq. 4): the SSA result O' is blended in the prefill epilogue and never written to HBM,
+ *   args->o <- o_hat = fma(alpha, o_full, (1 - alpha) * O')   with O' in fp32 before rounding,
+ * so alpha = 0 gives exactly ssa_prefill's bf16 output and alpha = 1 gives o_full; and, if d_o_hat
+ * and d_alpha_dev are non-NULL,
+ *   d_alpha = sum_e d_o_hat[e] * (o_full[e] - O'[e])
+ * (per thread fp32 per 128 outputs, then fp64; per-CTA fp64 partials; final fixed-order fp64 sum:
+ * deterministic). o_full and d_o_hat use o's layout and strides ([B, n_q, H, d_v], rows contiguous).
+ * bf16 in and out, the absorbed MLA shape only (else LOZA_ERR_UNSUPPORTED); same validation as
+ * ssa_prefill; o_full / d_o_hat 16-byte aligned (LOZA_ERR_SHAPE). alpha out of [0, 1] or NaN: the
+ * output is computed with that alpha, LOZA_ERR_INVALID goes to status_dev (if non-NULL) and NaN to
+ * d_alpha. ws: loza_workspace_size(LOZA_WS_BLEND, ...) bytes, required when d_alpha_dev != NULL. */
+loza_status_t ssa_prefill_blend(const loza_attn_args_t* args, loza_pattern_t pattern, const void* o_full,
+                                const float* alpha_dev, const void* d_o_hat, double* d_alpha_dev,
+                                int32_t* status_dev, void* ws, size_t ws_bytes, loza_stream_t stream);
+
 /* Sequence-parallel SSA prefill (north star; "uniform compute across
  * all ranks"). Rank r of `world` owns the contiguous, block-aligned shard of one
  * sequence at positions [q_start, q_start + n_local) with n_local = args->n_q,

@@ -187,6 +187,34 @@ loza_status_t loza_blend(const void* o_full, const void* o_sparse, const float* 
                      "blend launch");
 }
 
+loza_status_t ssa_prefill_blend(const loza_attn_args_t* args, loza_pattern_t pattern, const void* o_full,
+                                const float* alpha_dev, const void* d_o_hat, double* d_alpha_dev,
+                                int32_t* status_dev, void* ws, size_t ws_bytes, loza_stream_t stream) {
+  g_last_error[0] = 0;
+  if (!alpha_dev) return fail(LOZA_ERR_INVALID, "alpha_dev is NULL");
+  if (!o_full) return fail(LOZA_ERR_INVALID, "o_full is NULL");
+  if ((d_o_hat == nullptr) != (d_alpha_dev == nullptr))
+    return fail(LOZA_ERR_INVALID, "d_o_hat and d_alpha_dev must be both NULL or both set");
+  AttnProblem p;
+  loza_status_t rc = make_problem(args, true, pattern, nullptr, &p);
+  if (rc != LOZA_OK) return rc;
+  if (args->in_dtype != LOZA_BF16 || args->out_dtype != LOZA_BF16)
+    return fail(LOZA_ERR_UNSUPPORTED, "ssa_prefill_blend: bf16 in and out only");
+  Path path;
+  rc = choose_path(args, p, &path);
+  if (rc != LOZA_OK) return rc;
+  if (path != Path::kTc) return fail(LOZA_ERR_UNSUPPORTED, "ssa_prefill_blend: tensor-core path only");
+  if (!aligned16(o_full) || (d_o_hat && !aligned16(d_o_hat)))
+    return fail(LOZA_ERR_SHAPE, "o_full / d_o_hat must be 16-byte aligned");
+  if (d_alpha_dev && (!ws || ws_bytes < blend_ws_bytes() || (size_t)device_sm_count() * 8 > ws_bytes))
+    return fail(LOZA_ERR_INVALID, "workspace too small (%zu < %zu)", ws_bytes, blend_ws_bytes());
+  CalibArgs c{o_full, d_o_hat, alpha_dev, d_alpha_dev ? reinterpret_cast<double*>(ws) : nullptr, d_alpha_dev,
+              status_dev};
+  p.calib = &c;
+  if ((int64_t)p.batch * p.n_q * p.heads == 0) return LOZA_OK;
+  return cuda_status(launch_prefill_tc(p, (cudaStream_t)stream), "prefill_tc (calibration) launch");
+}
+
 loza_status_t ssa_select_blocks(int64_t n_q, int64_t q_start, loza_pattern_t pat, int32_t causal, int32_t* idx_dev,
                                 int32_t* count_dev, loza_stream_t stream) {
   g_last_error[0] = 0;

@@ -46,6 +46,15 @@ namespace loza {
 namespace {
 using namespace sm100;
 
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* ptr) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr));
+  return r;
+}
 #define FULL_L(slot) (full_l + 8 * (slot))
 #define QFULL_L(c) (qfull_l + 8 * (c))
 constexpr int kDqk = 576, kDv = 512, kChunks = 9;
@@ -110,6 +119,12 @@ struct PrefillParams {
   int32_t out_bf16;
   float* lse;
   int64_t units_per_batch, total_units;
+  // fused calibration forward (Eq. 3 in the epilogue; CalibArgs): o receives o_hat
+  const uint8_t* o_full;   // NULL: plain prefill
+  const uint8_t* d_o_hat;  // NULL: forward only
+  const float* alpha;
+  double* part;            // per-CTA fp64 partial of d_alpha
+  int32_t* status;
   int32_t small;              // all index math fits in uint32 (make_unit fast path)
   unsigned long long* trace;  // debug timeline (cluster 0, leader CTA), NULL in production
 };
@@ -192,6 +207,9 @@ __device__ __forceinline__ int64_t unit_index(const PrefillParams& p, int64_t it
     if (p.trace && cid == 0 && rank == 0 && (idx) < 64 && lane == 0) p.trace[(slot)*64 + (idx)] = clock64(); \
   } while (0)
 
+// kCalib: fused calibration forward (Eq. 3 in the epilogue); a separate instantiation so the plain
+// prefill keeps its register allocation
+template <bool kCalib>
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     prefill_tc_kernel(const __grid_constant__ PrefillParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -319,6 +337,17 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                            QFULL_L(c), pol_q);
         }
         __syncwarp();
+      }
+      if constexpr (kCalib) {
+        // this unit's O and d_o_hat rows (64 x 1 KB each per CTA, contiguous) into L2 ahead of the epilogue,
+        // which would otherwise wait a full HBM latency per 64-byte chunk it reads
+        const int64_t r0 = U.row0 + 64 * rank, rows_b = (int64_t)p.n_q * p.heads;
+        const int64_t nl = ((rows_b - r0 < 64 ? rows_b - r0 : 64) * kDv * 2) / 128;
+        const int64_t off = ((int64_t)U.bi * p.o_sb + r0 * kDv) * 2;
+        for (int64_t ln = lane; ln < nl; ln += 32) {
+          asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.o_full + off + ln * 128));
+          if (p.d_o_hat) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.d_o_hat + off + ln * 128));
+        }
       }
       load_k(U, 0);
       for (int i = 1; i < U.n_tiles; ++i) {
@@ -488,6 +517,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     const int64_t n_kv = p.n_kv;
     constexpr uint32_t kSmThreads = 32 * kSoftmaxWarps;
     uint32_t g = 0, uc = 0;
+    constexpr bool calib = kCalib;
+    const float alpha = calib ? *p.alpha : 0.f, om_alpha = 1.f - alpha;
+    double gacc = 0.0;  // this thread's part of d_alpha (fused calibration with d_o_hat)
     for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
       const Unit U = make_unit(p, unit_index(p, it));
       const int64_t row_g = U.row0 + 64 * rank + r;
@@ -607,14 +639,49 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         // between PV(T-1) and the next unit's first softmax): a flood of st.global from 256 threads queues
         // ahead of the MMA warp's mbarrier operations and stalls the tensor pipe at every unit boundary.
         uint32_t w[64];
+        if constexpr (!calib) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t ov[32];
-          tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ov);
-          tmem_wait_ld();
+          for (int c = 0; c < 4; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ov);
+            tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            w[16 * c + j] = pack_bf16x2(__uint_as_float(ov[2 * j]) * inv, __uint_as_float(ov[2 * j + 1]) * inv);
+            for (int j = 0; j < 16; ++j)
+              w[16 * c + j] = pack_bf16x2(__uint_as_float(ov[2 * j]) * inv, __uint_as_float(ov[2 * j + 1]) * inv);
+          }
+        } else {
+          // Eq. 3 on this thread's 128 outputs: o_hat = fma(alpha, O, (1 - alpha) O') with O' the fp32 SSA
+          // result (alpha = 0 gives exactly the plain bf16 output, alpha = 1 gives O), and
+          // d_alpha += d_o_hat (O - O'). O and d_o_hat are read straight from global (bf16, 64 B per chunk).
+          const int64_t off = ((int64_t)U.bi * p.o_sb + row_g * kDv + 256 * (int)ch + 128 * (int)kh) * 2;
+          const uint8_t* ofb = p.o_full + off;
+          const uint8_t* dhb = p.d_o_hat ? p.d_o_hat + off : nullptr;
+          float gs = 0.f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ov);
+            uint32_t xw[16], dw[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 x4 = row_ok ? ldg_nc_v4(ofb + 64 * c + 16 * q) : make_uint4(0, 0, 0, 0);
+              const uint4 d4 = (row_ok && dhb) ? ldg_nc_v4(dhb + 64 * c + 16 * q) : make_uint4(0, 0, 0, 0);
+              xw[4 * q] = x4.x; xw[4 * q + 1] = x4.y; xw[4 * q + 2] = x4.z; xw[4 * q + 3] = x4.w;
+              dw[4 * q] = d4.x; dw[4 * q + 1] = d4.y; dw[4 * q + 2] = d4.z; dw[4 * q + 3] = d4.w;
+            }
+            tmem_wait_ld();
+            uint32_t wc[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float y0 = __uint_as_float(ov[2 * j]) * inv, y1 = __uint_as_float(ov[2 * j + 1]) * inv;
+              const float x0 = bf_lo(xw[j]), x1 = bf_hi(xw[j]);
+              wc[j] = pack_bf16x2(fmaf(alpha, x0, om_alpha * y0), fmaf(alpha, x1, om_alpha * y1));
+              gs = fmaf(bf_lo(dw[j]), x0 - y0, fmaf(bf_hi(dw[j]), x1 - y1, gs));
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) w[16 * c + j] = wc[j];
+          }
+          gacc += (double)gs;
         }
         tc_fence_before();
         __syncwarp();
@@ -673,6 +740,21 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       g += U.n_tiles;
     }
     if (warp == 2 && lane == 0) bulk_wait_group0();  // output stores complete before exit
+    if (kCalib && p.part) {  // d_alpha: fixed-order per-CTA fp64 partial (deterministic)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, o);
+      named_bar_sync(1, kSmThreads);  // red[] is free: every unit's exchanges are done
+      double* wsum = reinterpret_cast<double*>(red);
+      if (lane == 0) wsum[warp - 2] = gacc;
+      named_bar_sync(1, kSmThreads);
+      if (threadIdx.x == 64) {
+        double t = 0.0;
+        for (int i = 0; i < (int)kSoftmaxWarps; ++i) t += wsum[i];
+        p.part[blockIdx.x] = t;
+      }
+    }
+    if (kCalib && p.status && blockIdx.x == 0 && threadIdx.x == 64)
+      *p.status = (alpha >= 0.f && alpha <= 1.f) ? LOZA_OK : LOZA_ERR_INVALID;
   }
   __syncwarp();
   tc_fence_before();
@@ -705,6 +787,13 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
   p.o_sb = a.o_sb;
   p.out_bf16 = a.out_bf16;
   p.lse = a.lse;
+  if (a.calib) {
+    p.o_full = reinterpret_cast<const uint8_t*>(a.calib->o_full);
+    p.d_o_hat = reinterpret_cast<const uint8_t*>(a.calib->d_o_hat);
+    p.alpha = a.calib->alpha;
+    p.part = a.calib->part;
+    p.status = a.calib->status;
+  }
   const int64_t rows = (int64_t)a.n_q * a.heads;
   p.units_per_batch = (rows + 127) / 128;
   p.trace = g_debug_trace;
@@ -726,16 +815,24 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
+    cudaError_t e = cudaFuncSetAttribute(prefill_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(prefill_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int sms = device_sm_count();
   int64_t ncl = sms / 2;
   if (ncl > p.total_units) ncl = p.total_units;
-  prefill_tc_kernel<<<(unsigned)(2 * ncl), kThreads, kSmemAlloc, st>>>(p);
+  if (a.calib)
+    prefill_tc_kernel<true><<<(unsigned)(2 * ncl), kThreads, kSmemAlloc, st>>>(p);
+  else
+    prefill_tc_kernel<false><<<(unsigned)(2 * ncl), kThreads, kSmemAlloc, st>>>(p);
   count_launch();
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && a.calib && a.calib->part)
+    e = launch_dalpha_reduce(a.calib->part, (int)(2 * ncl), a.calib->alpha, a.calib->d_alpha, st);
+  return e;
 }
 
 }  // namespace loza

@@ -134,6 +134,12 @@ cudaError_t launch_t(const void* of, const void* os, const float* alpha, void* o
 
 size_t blend_ws_bytes() { return sizeof(double) * kMaxBlocks; }
 
+cudaError_t launch_dalpha_reduce(const double* part, int n, const float* alpha, double* out, cudaStream_t st) {
+  dalpha_reduce_kernel<<<1, 256, 0, st>>>(part, n, alpha, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_blend(const void* o_full, const void* o_sparse, const float* alpha, void* o_hat,
                          const void* d_o_hat, double* d_alpha, int64_t numel, int bf16, int32_t* status,
                          void* ws, cudaStream_t st) {

@@ -23,6 +23,16 @@ struct KvView {
   KvSeg seg[3];
 };
 
+// fused calibration forward (ssa_prefill_blend): Eq. 3 applied in the SSA prefill epilogue
+struct CalibArgs {
+  const void* o_full;   // [B, n_q, H, d_v] bf16, o's layout
+  const void* d_o_hat;  // same layout, nullable (forward only)
+  const float* alpha;   // device scalar
+  double* part;         // per-CTA fp64 partials of d_alpha (>= SM count entries), NULL without d_o_hat
+  double* d_alpha;      // device scalar out, NULL without d_o_hat
+  int32_t* status;      // nullable: LOZA_ERR_INVALID if alpha is not in [0, 1]
+};
+
 struct AttnProblem {
   int32_t batch, n_q, heads, d_qk, d_v;
   int64_t n_kv, q_start;
@@ -37,6 +47,7 @@ struct AttnProblem {
   float* lse;
   const int32_t* seq_lens;  // non-NULL => decode (one query at seq_len-1)
   KvView kv;
+  const CalibArgs* calib = nullptr;  // non-NULL => fused blend epilogue (bf16 SSA prefill only)
 };
 
 // launchers (return cudaError_t of the launch)
@@ -47,6 +58,8 @@ cudaError_t launch_blend(const void* o_full, const void* o_sparse, const float* 
                          const void* d_o_hat, double* d_alpha, int64_t numel, int bf16, int32_t* status,
                          void* ws, cudaStream_t st);
 size_t blend_ws_bytes();
+// fixed-order fp64 sum of n per-CTA partials; NaN if alpha is not in [0, 1] (blend.cu)
+cudaError_t launch_dalpha_reduce(const double* part, int n, const float* alpha, double* out, cudaStream_t st);
 // tcgen05 paths (bf16, d_qk 576, d_v 512)
 cudaError_t launch_prefill_tc(const AttnProblem& p, cudaStream_t st);
 cudaError_t launch_decode_tc(const AttnProblem& p, void* ws, size_t ws_bytes, cudaStream_t st);

@@ -23,7 +23,7 @@ STATUS = {0: "LOZA_OK", 1: "LOZA_ERR_INVALID", 2: "LOZA_ERR_SHAPE", 3: "LOZA_ERR
           4: "LOZA_ERR_CUDA", 5: "LOZA_ERR_NCCL"}
 
 PAPER_PATTERN = (1, 7, 128)  # (s, l, b)
-EXPORTS = ["ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_seqpar_prefill",
+EXPORTS = ["ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_prefill_blend", "ssa_seqpar_prefill",
            "loza_seqpar_prefill_local", "ssa_select_blocks", "loza_workspace_size", "loza_status_string",
            "loza_last_error", "loza_kernel_launches", "loza_num_sms"]
 
@@ -67,6 +67,7 @@ def lib():
         L.ssa_decode.argtypes = [P(AttnArgs), V, Pattern, V, SZ, V]
         L.full_attn_ref.argtypes = [P(AttnArgs), V, V, SZ, V]
         L.loza_blend.argtypes = [V, V, V, V, V, V, I64, S, V, V, SZ, V]
+        L.ssa_prefill_blend.argtypes = [P(AttnArgs), Pattern, V, V, V, V, V, V, SZ, V]
         L.ssa_seqpar_prefill.argtypes = [P(AttnArgs), Pattern, V, I32, I32, V, SZ, V]
         L.loza_seqpar_prefill_local.argtypes = [P(AttnArgs), Pattern, I32, I32, V, V, V, V, V, SZ, V]
         L.ssa_select_blocks.argtypes = [I64, I64, Pattern, I32, V, V, V]
@@ -172,6 +173,34 @@ def ssa_prefill(q, k, v=None, pattern=PAPER_PATTERN, scale=None, *, d_v=512, out
     a = make_args(q, k, v, o, scale=scale, q_start=q_start, lse=lse)
     _check(lib().ssa_prefill(ctypes.byref(a), _pattern(pattern), _stream(stream)))
     return o
+
+
+def ssa_prefill_blend(q, k, o_full, alpha, d_o_hat=None, v=None, pattern=PAPER_PATTERN, scale=None, *, d_v=512,
+                      out=None, q_start=0, status=None, stream=None):
+    """Fused calibration forward (Eq. 3 with O' = SSA prefill, never stored): returns (o_hat, d_alpha or None).
+    alpha: 1-element fp32 CUDA tensor; o_full / d_o_hat: bf16, o's shape [.., n_q, H, d_v]."""
+    k, v = _split_kv(k, v, d_v)
+    scale = default_scale(q.shape[-1]) if scale is None else scale
+    o = out if out is not None else _alloc_out(q, v.shape[-1], torch.bfloat16)
+    assert o_full.shape == o.shape and o_full.dtype == torch.bfloat16 and o_full.is_contiguous()
+    assert alpha.dtype == torch.float32 and alpha.is_cuda
+    a = make_args(q, k, v, o, scale=scale, q_start=q_start)
+    d_alpha = None
+    if d_o_hat is not None:
+        assert d_o_hat.shape == o.shape and d_o_hat.dtype == torch.bfloat16 and d_o_hat.is_contiguous()
+        d_alpha = torch.empty(1, dtype=torch.float64, device=q.device)
+    need = lib().loza_workspace_size(LOZA_WS_BLEND, None, Pattern(0, 1, 1), 1)
+    dev = q.device
+    ws = _blend_ws.get(dev)
+    if ws is None:
+        ws = _blend_ws[dev] = torch.empty(need, dtype=torch.uint8, device=dev)
+    V = ctypes.c_void_p
+    _check(lib().ssa_prefill_blend(ctypes.byref(a), _pattern(pattern), V(o_full.data_ptr()), V(alpha.data_ptr()),
+                                   V(d_o_hat.data_ptr() if d_o_hat is not None else 0),
+                                   V(d_alpha.data_ptr() if d_alpha is not None else 0),
+                                   V(status.data_ptr() if status is not None else 0), V(ws.data_ptr()), need,
+                                   _stream(stream)))
+    return o, d_alpha
 
 
 _decode_ws_cache = {}
