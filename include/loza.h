@@ -137,6 +137,31 @@ loza_status_t ssa_prefill_blend(const loza_attn_args_t* args, loza_pattern_t pat
                                 const float* alpha_dev, const void* d_o_hat, double* d_alpha_dev,
                                 int32_t* status_dev, void* ws, size_t ws_bytes, loza_stream_t stream);
 
+/* Bounded SSA KV cache. Per sequence R = (s+l)*b rows:
+ * the s sink blocks at rows [0, s*b) and a ring of l blocks, block kb >= s at rows
+ * s*b + ((kb - s) mod l)*b. Appending in position order evicts a local block exactly when it can no longer
+ * be attended (block-boundary eviction), so after positions [0, t) were appended the cache holds every key
+ * allowed for the query at t and nothing else; (s+l)*b*d*elem bytes per sequence whatever the context
+ * (B64 at 1M: 75 MB instead of 77 GB).
+ *
+ * ssa_ring_append: copy m new rows per sequence (rows [B, m, d], strides in elements) at absolute positions
+ * pos0_dev[b] .. pos0_dev[b] + m - 1 (pos0 = the sequence's length before the append, on the device) into
+ * `cache` [B, (s+l)*b, d]. Rows evicted within the same append are skipped (a whole prompt is appended with
+ * m = n, pos0 = 0). d*elem must be a multiple of 16 and base pointers / strides 16-byte aligned
+ * (LOZA_ERR_SHAPE). */
+loza_status_t ssa_ring_append(const void* rows, int64_t rows_stride_b, int64_t rows_stride_tok, int32_t m,
+                              const int32_t* pos0_dev, loza_pattern_t pattern, void* cache, int64_t cache_stride_b,
+                              int64_t cache_stride_tok, int32_t batch, int32_t d, loza_dtype_t dtype,
+                              loza_stream_t stream);
+
+/* ssa_decode over the bounded ring cache: args->k / args->v point into the ring cache, args->n_kv must be
+ * (s+l)*b; seq_lens_dev are absolute lengths (any value >= 1: the ring holds the window of position
+ * seq_len - 1 once positions [0, seq_len) were appended). Bitwise identical to ssa_decode over a contiguous
+ * cache with the same rows. bf16, 64 heads, b % 128 == 0 and 2*batch <= SM count (the CTA-pair kernel);
+ * else LOZA_ERR_UNSUPPORTED. No workspace. */
+loza_status_t ssa_decode_ring(const loza_attn_args_t* args, const int32_t* seq_lens_dev, loza_pattern_t pattern,
+                              loza_stream_t stream);
+
 /* Sequence-parallel SSA prefill (north star; "uniform compute across
  * all ranks"). Rank r of `world` owns the contiguous, block-aligned shard of one
  * sequence at positions [q_start, q_start + n_local) with n_local = args->n_q,

@@ -215,6 +215,45 @@ loza_status_t ssa_prefill_blend(const loza_attn_args_t* args, loza_pattern_t pat
   return cuda_status(launch_prefill_tc(p, (cudaStream_t)stream), "prefill_tc (calibration) launch");
 }
 
+loza_status_t ssa_ring_append(const void* rows, int64_t rows_stride_b, int64_t rows_stride_tok, int32_t m,
+                              const int32_t* pos0_dev, loza_pattern_t pat, void* cache, int64_t cache_stride_b,
+                              int64_t cache_stride_tok, int32_t batch, int32_t d, loza_dtype_t dtype,
+                              loza_stream_t stream) {
+  g_last_error[0] = 0;
+  if (pat.sink_blocks < 0 || pat.local_blocks < 1 || pat.block_size < 1) return fail(LOZA_ERR_INVALID, "bad pattern");
+  if (dtype != LOZA_F32 && dtype != LOZA_BF16) return fail(LOZA_ERR_INVALID, "unknown dtype");
+  if (m < 0 || batch < 0 || d < 1) return fail(LOZA_ERR_SHAPE, "bad m / batch / d");
+  if ((int64_t)m * batch == 0) return LOZA_OK;
+  if (!rows || !cache || !pos0_dev) return fail(LOZA_ERR_INVALID, "NULL pointer");
+  const int64_t esz = dtype == LOZA_BF16 ? 2 : 4;
+  if ((d * esz) % 16 || !aligned16(rows) || !aligned16(cache) || (rows_stride_b * esz) % 16 ||
+      (rows_stride_tok * esz) % 16 || (cache_stride_b * esz) % 16 || (cache_stride_tok * esz) % 16)
+    return fail(LOZA_ERR_SHAPE, "ring append needs 16-byte rows, pointers and strides");
+  return cuda_status(launch_ring_append(rows, rows_stride_b * esz, rows_stride_tok * esz, m, pos0_dev,
+                                        pat.sink_blocks, pat.local_blocks, pat.block_size, cache, cache_stride_b * esz,
+                                        cache_stride_tok * esz, batch, (int32_t)(d * esz), (cudaStream_t)stream),
+                     "ring append launch");
+}
+
+loza_status_t ssa_decode_ring(const loza_attn_args_t* args, const int32_t* seq_lens_dev, loza_pattern_t pattern,
+                              loza_stream_t stream) {
+  g_last_error[0] = 0;
+  if (!seq_lens_dev) return fail(LOZA_ERR_INVALID, "seq_lens_dev is NULL");
+  AttnProblem p;
+  loza_status_t rc = make_problem(args, true, pattern, seq_lens_dev, &p);
+  if (rc != LOZA_OK) return rc;
+  if (args->n_kv != (int64_t)(pattern.sink_blocks + pattern.local_blocks) * pattern.block_size)
+    return fail(LOZA_ERR_SHAPE, "ring cache: n_kv must be (s+l)*b");
+  if ((int64_t)p.batch * p.heads == 0) return LOZA_OK;
+  Path path;
+  rc = choose_path(args, p, &path);
+  if (rc != LOZA_OK) return rc;
+  if (path != Path::kTc || !decode_pair_eligible(p, device_sm_count()))
+    return fail(LOZA_ERR_UNSUPPORTED, "ring decode: bf16, H == 64, b %% 128 == 0, 2*batch <= SMs");
+  p.ring = 1;
+  return cuda_status(launch_decode_pair(p, (cudaStream_t)stream), "decode_pair (ring) launch");
+}
+
 loza_status_t ssa_select_blocks(int64_t n_q, int64_t q_start, loza_pattern_t pat, int32_t causal, int32_t* idx_dev,
                                 int32_t* count_dev, loza_stream_t stream) {
   g_last_error[0] = 0;

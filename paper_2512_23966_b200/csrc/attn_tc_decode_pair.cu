@@ -70,6 +70,7 @@ struct PairParams {
   CUtensorMap q_map, k_map, v_map, o_map;
   const int32_t* seq_lens;
   int32_t batch, s, l, b;
+  int32_t ring;  // k/v is the bounded ring cache (ring_cache.cu): tile rows are remapped, positions are not
   int64_t t_cap;
   float scale_log2;
   void* o;
@@ -106,6 +107,13 @@ __device__ __forceinline__ SeqTiles seq_tiles(const PairParams& p, int bi) {
 }
 __device__ __forceinline__ int32_t tile_k0(const SeqTiles& t, int i) {
   return (i < t.n_sink ? i : t.loc_begin + (i - t.n_sink)) * 128;
+}
+// cache row of the 128-key tile at absolute key k0: identity, or the ring slot of its block
+__device__ __forceinline__ int32_t kv_row(const PairParams& p, int32_t k0) {
+  if (!p.ring) return k0;
+  const int32_t kb = k0 / p.b;
+  if (kb < p.s) return k0;
+  return p.s * p.b + ((kb - p.s) % p.l) * p.b + (k0 - kb * p.b);
 }
 
 #define DTRACE(slot, idx)                                                                        \
@@ -235,12 +243,12 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           next();
         }
     };
-    load_k(tile_k0(st, t0));
+    load_k(kv_row(p, tile_k0(st, t0)));
     for (int i = t0 + 1; i < t1; ++i) {
-      load_k(tile_k0(st, i));
-      load_v(tile_k0(st, i - 1));
+      load_k(kv_row(p, tile_k0(st, i)));
+      load_v(kv_row(p, tile_k0(st, i - 1)));
     }
-    load_v(tile_k0(st, t1 - 1));
+    load_v(kv_row(p, tile_k0(st, t1 - 1)));
   } else if (warp == 1 && has_tiles) {
     // ----------------------------------------------------- UMMA issuer (warp-uniform, elected lane issues)
     constexpr uint32_t idesc_s = idesc_bf16_f32(128, 64, false, false);
@@ -557,7 +565,8 @@ cudaError_t launch_decode_pair(const AttnProblem& a, cudaStream_t st) {
   p.s = a.s;
   p.l = a.l;
   p.b = a.b;
-  p.t_cap = a.n_kv;
+  p.ring = a.ring;
+  p.t_cap = a.ring ? (int64_t)0x7FFFFFFF : a.n_kv;  // ring: positions are absolute, any length
   p.scale_log2 = a.scale * 1.4426950408889634f;
   p.o = a.o;
   p.o_sb = a.o_sb;

@@ -48,6 +48,7 @@ struct AttnProblem {
   const int32_t* seq_lens;  // non-NULL => decode (one query at seq_len-1)
   KvView kv;
   const CalibArgs* calib = nullptr;  // non-NULL => fused blend epilogue (bf16 SSA prefill only)
+  int32_t ring = 0;                  // decode: k/v is the bounded ring cache of ring_cache.cu (n_kv = (s+l)*b)
 };
 
 // launchers (return cudaError_t of the launch)
@@ -66,6 +67,9 @@ cudaError_t launch_decode_tc(const AttnProblem& p, void* ws, size_t ws_bytes, cu
 size_t decode_tc_ws_bytes(const AttnProblem& p);
 bool decode_pair_eligible(const AttnProblem& a, int sms);
 cudaError_t launch_decode_pair(const AttnProblem& a, cudaStream_t st);
+cudaError_t launch_ring_append(const void* rows, int64_t r_sb, int64_t r_st, int32_t m, const int32_t* pos0,
+                               int32_t s, int32_t l, int32_t b, void* cache, int64_t c_sb, int64_t c_st,
+                               int32_t batch, int32_t row_bytes, cudaStream_t st);
 
 void count_launch(uint64_t n = 1);
 loza_status_t fail(loza_status_t st, const char* fmt, ...);

@@ -23,7 +23,8 @@ STATUS = {0: "LOZA_OK", 1: "LOZA_ERR_INVALID", 2: "LOZA_ERR_SHAPE", 3: "LOZA_ERR
           4: "LOZA_ERR_CUDA", 5: "LOZA_ERR_NCCL"}
 
 PAPER_PATTERN = (1, 7, 128)  # (s, l, b)
-EXPORTS = ["ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_prefill_blend", "ssa_seqpar_prefill",
+EXPORTS = ["ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_prefill_blend", "ssa_ring_append",
+           "ssa_decode_ring", "ssa_seqpar_prefill",
            "loza_seqpar_prefill_local", "ssa_select_blocks", "loza_workspace_size", "loza_status_string",
            "loza_last_error", "loza_kernel_launches", "loza_num_sms"]
 
@@ -68,6 +69,8 @@ def lib():
         L.full_attn_ref.argtypes = [P(AttnArgs), V, V, SZ, V]
         L.loza_blend.argtypes = [V, V, V, V, V, V, I64, S, V, V, SZ, V]
         L.ssa_prefill_blend.argtypes = [P(AttnArgs), Pattern, V, V, V, V, V, V, SZ, V]
+        L.ssa_ring_append.argtypes = [V, I64, I64, I32, V, Pattern, V, I64, I64, I32, I32, S, V]
+        L.ssa_decode_ring.argtypes = [P(AttnArgs), V, Pattern, V]
         L.ssa_seqpar_prefill.argtypes = [P(AttnArgs), Pattern, V, I32, I32, V, SZ, V]
         L.loza_seqpar_prefill_local.argtypes = [P(AttnArgs), Pattern, I32, I32, V, V, V, V, V, SZ, V]
         L.ssa_select_blocks.argtypes = [I64, I64, Pattern, I32, V, V, V]
@@ -201,6 +204,39 @@ def ssa_prefill_blend(q, k, o_full, alpha, d_o_hat=None, v=None, pattern=PAPER_P
                                    V(status.data_ptr() if status is not None else 0), V(ws.data_ptr()), need,
                                    _stream(stream)))
     return o, d_alpha
+
+
+def ring_rows(pattern=PAPER_PATTERN) -> int:
+    s, l, b = pattern
+    return (s + l) * b
+
+
+def ssa_ring_append(cache, rows, pos0, pattern=PAPER_PATTERN, stream=None):
+    """Append rows [B, m, d] at absolute positions pos0[b] .. (int32 CUDA tensor [B]) to the ring cache
+    [B, (s+l)*b, d] (bounded SSA KV cache, block-boundary eviction)."""
+    assert cache.dim() == 3 and rows.dim() == 3 and rows.dtype == cache.dtype and rows.shape[-1] == cache.shape[-1]
+    assert cache.shape[1] == ring_rows(pattern) and pos0.dtype == torch.int32 and pos0.is_cuda
+    V = ctypes.c_void_p
+    _check(lib().ssa_ring_append(V(rows.data_ptr()), rows.stride(0), rows.stride(1), rows.shape[1],
+                                 V(pos0.data_ptr()), _pattern(pattern), V(cache.data_ptr()), cache.stride(0),
+                                 cache.stride(1), rows.shape[0], rows.shape[-1], _dt(rows), _stream(stream)))
+    return cache
+
+
+def ssa_decode_ring(q, cache, seq_lens, v=None, pattern=PAPER_PATTERN, scale=None, *, d_v=512, out=None, lse=None,
+                    out_dtype=None, stream=None):
+    """SSA decode over the bounded ring cache [B, (s+l)*b, d_qk]; seq_lens: absolute lengths (int32 CUDA [B])."""
+    q4 = q if q.dim() == 4 else q.unsqueeze(1)
+    k, v = _split_kv(cache, v, d_v)
+    scale = default_scale(q4.shape[-1]) if scale is None else scale
+    o = out if out is not None else torch.empty((*q4.shape[:3], v.shape[-1]), dtype=out_dtype or q4.dtype,
+                                                device=q4.device)
+    o4 = o if o.dim() == 4 else o.unsqueeze(1)
+    a = make_args(q4, k, v, o4, scale=scale, lse=lse)
+    assert seq_lens.dtype == torch.int32 and seq_lens.is_cuda
+    _check(lib().ssa_decode_ring(ctypes.byref(a), ctypes.c_void_p(seq_lens.data_ptr()), _pattern(pattern),
+                                 _stream(stream)))
+    return o if q.dim() == 4 else o4[:, 0]
 
 
 _decode_ws_cache = {}
