@@ -87,7 +87,9 @@ constexpr int kBarSFree = kBarSFull + 2;         // [2]
 constexpr int kBarPFull = kBarSFree + 2;         // [1]
 constexpr int kBarOFull = kBarPFull + 1;         // [2]
 constexpr int kBarOFree = kBarOFull + 2;
-constexpr int kNumBars = kBarOFree + 1;
+constexpr int kBarOfFull = kBarOFree + 1;   // calibration: O_full of the unit staged in the Q region (local)
+constexpr int kBarOfEmpty = kBarOfFull + 1;  // calibration: the epilogue has read it (8 softmax warps, local)
+constexpr int kNumBars = kBarOfEmpty + 1;
 constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
 constexpr int kOffPub = kOffTmemPtr + 4;                // uint32 [2]: producers' next ring positions
 constexpr int kOffRed = (kOffPub + 8 + 15) & ~15;  // float [2 buf][4 quarter-rows][64]; epilogue reuses it
@@ -107,6 +109,7 @@ struct PrefillParams {
   CUtensorMap k2_map[3];  // 4-D, box 128 rows x 2 chunks
   CUtensorMap v_map[3];   // 4-D, box 128 rows x 2 chunks
   CUtensorMap o_map;      // bf16 output, box 64 rows x 64 dims (TMA-store epilogue)
+  CUtensorMap of_map;     // calibration: O_full, same boxes (staged in the Q region for the epilogue)
   int64_t seg_begin[3];
   int32_t seg_len[3];
   int32_t nseg;
@@ -240,6 +243,8 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     }
     mbar_init(bar(kBarPFull), kArrivalsPerPair);
     mbar_init(bar(kBarOFree), kArrivalsPerPair);
+    mbar_init(bar(kBarOfFull), 1);
+    mbar_init(bar(kBarOfEmpty), kSoftmaxWarps);
     reinterpret_cast<volatile uint32_t*>(smem + kOffPub)[0] = 0;
     reinterpret_cast<volatile uint32_t*>(smem + kOffPub)[1] = 0;
     fence_mbar_init();
@@ -327,8 +332,40 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       }
       ++gk;
     };
+    // calibration: once a unit's last S has released the Q region, the unit's O_full rows are staged there
+    // (8 boxes [64 rows x 64 dims], TMA) for the epilogue; the next unit's Q follows the epilogue's release
+    Unit Uprev;
+    auto stage_o_full = [&](const Unit& Us, uint32_t ucs) {
+      for (int c = 0; c < kChunks; ++c) mbar_wait(bar(kBarQEmpty + c), ucs & 1);  // unit ucs's last S is done
+      if (elect_one()) {
+        mbar_arrive_expect_tx(bar(kBarOfFull), 8 * 8192);
+        for (int m = 0; m < 8; ++m)
+          tma_load_3d(sbase + kOffQ + m * 8192, &p.of_map, 64 * m, (int32_t)(Us.row0 + 64 * rank), Us.bi,
+                      bar(kBarOfFull), pol_q);
+      }
+      __syncwarp();
+    };
     for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
       const Unit U = make_unit(p, unit_index(p, it));
+      // Before blocking outside acquire(): publish the next ring position (all items before it are issued or
+      // the V producer's), else the V producer's handshake for the previous unit's last V items waits on this
+      // warp while this warp waits (here, or in the calibration OfEmpty wait) on work that needs those items.
+      if (lane == 0) pub[0] = rp.pos;
+      __syncwarp();
+      if constexpr (kCalib) {
+        if (uc > 0) {
+          stage_o_full(Uprev, uc - 1);
+          mbar_wait(bar(kBarOfEmpty), (uc - 1) & 1);  // the previous unit's epilogue has read it
+        }
+        // d_o_hat rows of this unit into L2 ahead of the epilogue (read with plain loads there)
+        if (p.d_o_hat) {
+          const int64_t r0 = U.row0 + 64 * rank, rows_b = (int64_t)p.n_q * p.heads;
+          const int64_t nl = ((rows_b - r0 < 64 ? rows_b - r0 : 64) * kDv * 2) / 128;
+          const int64_t off = ((int64_t)U.bi * p.o_sb + r0 * kDv) * 2;
+          for (int64_t ln = lane; ln < nl; ln += 32)
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.d_o_hat + off + ln * 128));
+        }
+      }
       for (int c = 0; c < kChunks; ++c) {
         mbar_wait(bar(kBarQEmpty + c), (uc & 1) ^ 1);
         if (elect_one()) {
@@ -338,17 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         }
         __syncwarp();
       }
-      if constexpr (kCalib) {
-        // this unit's O and d_o_hat rows (64 x 1 KB each per CTA, contiguous) into L2 ahead of the epilogue,
-        // which would otherwise wait a full HBM latency per 64-byte chunk it reads
-        const int64_t r0 = U.row0 + 64 * rank, rows_b = (int64_t)p.n_q * p.heads;
-        const int64_t nl = ((rows_b - r0 < 64 ? rows_b - r0 : 64) * kDv * 2) / 128;
-        const int64_t off = ((int64_t)U.bi * p.o_sb + r0 * kDv) * 2;
-        for (int64_t ln = lane; ln < nl; ln += 32) {
-          asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.o_full + off + ln * 128));
-          if (p.d_o_hat) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.d_o_hat + off + ln * 128));
-        }
-      }
+      if constexpr (kCalib) Uprev = U;
       load_k(U, 0);
       for (int i = 1; i < U.n_tiles; ++i) {
         load_k(U, i);
@@ -357,6 +384,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       rp.skip(kVItems);
     }
     if (lane == 0) pub[0] = 0xFFFFFFFFu;
+    if constexpr (kCalib) {
+      if (uc > 0) stage_o_full(Uprev, uc - 1);
+    }
   } else if (warp == kVWarp) {
     // ===================================================== V items producer (both CTAs)
     const uint64_t pol_kv = policy_evict_last();
@@ -654,17 +684,19 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           // result (alpha = 0 gives exactly the plain bf16 output, alpha = 1 gives O), and
           // d_alpha += d_o_hat (O - O'). O and d_o_hat are read straight from global (bf16, 64 B per chunk).
           const int64_t off = ((int64_t)U.bi * p.o_sb + row_g * kDv + 256 * (int)ch + 128 * (int)kh) * 2;
-          const uint8_t* ofb = p.o_full + off;
           const uint8_t* dhb = p.d_o_hat ? p.d_o_hat + off : nullptr;
           float gs = 0.f;
+          mbar_wait(bar(kBarOfFull), uc & 1);  // this unit's O_full rows, staged in the Q region
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t ov[32];
             tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ov);
             uint32_t xw[16], dw[16];
+            // O_full box m = dims [64 m, +64): row r at m * 8192 + 128 r, 16-B units swizzled by r & 7
+            const uint8_t* ofs = smem + kOffQ + (4 * ch + 2 * kh + (c >> 1)) * 8192 + r * 128;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const uint4 x4 = row_ok ? ldg_nc_v4(ofb + 64 * c + 16 * q) : make_uint4(0, 0, 0, 0);
+              const uint4 x4 = *reinterpret_cast<const uint4*>(ofs + ((((c & 1) * 4 + q) ^ (r & 7)) << 4));
               const uint4 d4 = (row_ok && dhb) ? ldg_nc_v4(dhb + 64 * c + 16 * q) : make_uint4(0, 0, 0, 0);
               xw[4 * q] = x4.x; xw[4 * q + 1] = x4.y; xw[4 * q + 2] = x4.z; xw[4 * q + 3] = x4.w;
               dw[4 * q] = d4.x; dw[4 * q + 1] = d4.y; dw[4 * q + 2] = d4.z; dw[4 * q + 3] = d4.w;
@@ -681,6 +713,8 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) w[16 * c + j] = wc[j];
           }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_local(bar(kBarOfEmpty));  // the staged O_full may be replaced by Q
           gacc += (double)gs;
         }
         tc_fence_before();
@@ -788,6 +822,8 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
   p.out_bf16 = a.out_bf16;
   p.lse = a.lse;
   if (a.calib) {
+    if (!encode_3d(&p.of_map, a.calib->o_full, kDv, (uint64_t)a.n_q * a.heads, a.batch, kDv, a.o_sb, 64))
+      return cudaErrorInvalidValue;
     p.o_full = reinterpret_cast<const uint8_t*>(a.calib->o_full);
     p.d_o_hat = reinterpret_cast<const uint8_t*>(a.calib->d_o_hat);
     p.alpha = a.calib->alpha;
