@@ -60,6 +60,10 @@ def lib():
         L.loza_oracle_blend.restype = None
         L.loza_oracle_blend.argtypes = [_f32p, _f32p, _dbl, ctypes.c_void_p, _i64, ctypes.c_void_p,
                                         ctypes.c_void_p]
+        L.loza_oracle_attention_backward.restype = None
+        L.loza_oracle_attention_backward.argtypes = [_f32p, _i64p, _i64, _i64, _f32p, _i64, _f32p, _i64, _f32p,
+                                                     _i64, _i64, _i32, _i32, _dbl, _i32, _i32, _i32, _i32, _i32,
+                                                     _f64p, _f64p, _f64p]
         L.loza_oracle_num_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -127,6 +131,23 @@ def attention_rows(q_rows, pos, k, v, scale: float, s: int = 1, l: int = 7, b: i
     lib().loza_oracle_attention_rows(q_rows, pos, R, dqk, k, k.shape[1], v, dv, n_kv, dqk, dv, float(scale),
                                      s, l, b, int(sparse), int(causal), o, lse)
     return o, lse[:R]
+
+
+def attention_backward(q_rows, pos, k, v, do_rows, scale: float, s: int = 1, l: int = 7, b: int = 128,
+                       sparse: bool = True, causal: bool = True):
+    """Backward of attention_rows for the loss with dL/dO = do_rows: returns (dq [R,dqk], dk [n_kv,dqk],
+    dv [n_kv,dv]) in fp64."""
+    q_rows, k, v, do_rows = _c32(q_rows), _c32(k), _c32(v), _c32(do_rows)
+    pos = np.ascontiguousarray(pos, dtype=np.int64)
+    R, dqk = q_rows.shape
+    n_kv, dv = v.shape
+    assert k.shape[0] == n_kv and len(pos) == R and do_rows.shape == (R, dv)
+    dq = np.empty((max(R, 1), dqk), dtype=np.float64)
+    dk = np.empty((max(n_kv, 1), dqk), dtype=np.float64)
+    dvo = np.empty((max(n_kv, 1), dv), dtype=np.float64)
+    lib().loza_oracle_attention_backward(q_rows, pos, R, dqk, k, k.shape[1], v, dv, do_rows, dv, n_kv, dqk, dv,
+                                         float(scale), s, l, b, int(sparse), int(causal), dq, dk, dvo)
+    return dq[:R], dk[:n_kv], dvo[:n_kv]
 
 
 def attention(q, k, v, scale: float, pattern=None, causal: bool = True, q_start: int = 0):

@@ -34,6 +34,9 @@
  *                      invariance
  *   blend              endpoints, linearity / finite difference
  *
+ *   backward           central finite differences of L = sum dO.O through the forward
+ *                      oracle (fp64) on q, k, v entries; single key => dq = dk = 0,
+ *                      dv = sum dO; constant V => dq = dk = 0
  */
 #include <math.h>
 #include <stdint.h>
@@ -209,6 +212,92 @@ void loza_oracle_blend(const float* o, const float* op, double alpha, const floa
     for (int64_t e = 0; e < n; ++e) acc += (double)dohat[e] * ((double)o[e] - (double)op[e]);
     *dalpha = acc;
   }
+}
+
+/* Backward of Eq. 1 / Eq. 4 (softmax attention over the allowed keys), fp64, for R query rows at absolute
+ * positions pos[r] against one K/V sequence of n_kv rows. The chain rule of O_r = sum_j P_rj v_j with
+ * P_rj = exp(z_rj - m_r) / L_r and z_rj = scale q_r . k_j over the allowed j, for a loss with dL/dO_r = do_r:
+ *   dP_rj = do_r . v_j ;  D_r = sum_j P_rj dP_rj (= do_r . O_r) ;  dZ_rj = P_rj (dP_rj - D_r)
+ *   dq_r = scale sum_j dZ_rj k_j ;  dk_j = scale sum_r dZ_rj q_r ;  dv_j = sum_r P_rj do_r
+ * Pass 1 (rows): m_r, L_r, D_r and dq_r. Pass 2 (keys): dk_j, dv_j over the rows that allow j (no reduction
+ * races). dq [R][d_qk], dk [n_kv][d_qk], dv [n_kv][d_v] are written (fp64). */
+void loza_oracle_attention_backward(const float* q, const int64_t* pos, int64_t R, int64_t q_stride,
+                                    const float* k, int64_t k_stride, const float* v, int64_t v_stride,
+                                    const float* dout, int64_t do_stride, int64_t n_kv, int32_t d_qk,
+                                    int32_t d_v, double scale, int32_t s, int32_t l, int32_t b,
+                                    int32_t sparse, int32_t causal, double* dq, double* dk, double* dv) {
+  double* m = (double*)malloc(sizeof(double) * (size_t)(R > 0 ? R : 1));
+  double* L = (double*)malloc(sizeof(double) * (size_t)(R > 0 ? R : 1));
+  double* D = (double*)malloc(sizeof(double) * (size_t)(R > 0 ? R : 1));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t r = 0; r < R; ++r) {
+    uint8_t* mrow = (uint8_t*)malloc((size_t)(n_kv > 0 ? n_kv : 1));
+    double* z = (double*)malloc(sizeof(double) * (size_t)(n_kv > 0 ? n_kv : 1));
+    const float* qr = q + r * q_stride;
+    const float* dor = dout + r * do_stride;
+    loza_oracle_mask_row(pos[r], n_kv, s, l, b, sparse, causal, mrow);
+    double mx = -INFINITY;
+    for (int64_t j = 0; j < n_kv; ++j) {
+      if (!mrow[j]) continue;
+      const float* kj = k + j * k_stride;
+      double acc = 0.0;
+      for (int32_t d = 0; d < d_qk; ++d) acc += (double)qr[d] * (double)kj[d];
+      z[j] = scale * acc;
+      if (z[j] > mx) mx = z[j];
+    }
+    double Ls = 0.0;
+    for (int64_t j = 0; j < n_kv; ++j)
+      if (mrow[j]) Ls += exp(z[j] - mx);
+    double Dr = 0.0;  /* D_r = sum_j P_rj dP_rj */
+    for (int64_t j = 0; j < n_kv; ++j) {
+      if (!mrow[j]) continue;
+      const float* vj = v + j * v_stride;
+      double dp = 0.0;
+      for (int32_t d = 0; d < d_v; ++d) dp += (double)dor[d] * (double)vj[d];
+      Dr += exp(z[j] - mx) / Ls * dp;
+    }
+    double* dqr = dq + r * d_qk;
+    for (int32_t d = 0; d < d_qk; ++d) dqr[d] = 0.0;
+    for (int64_t j = 0; j < n_kv; ++j) {
+      if (!mrow[j]) continue;
+      const float* vj = v + j * v_stride;
+      const float* kj = k + j * k_stride;
+      double dp = 0.0;
+      for (int32_t d = 0; d < d_v; ++d) dp += (double)dor[d] * (double)vj[d];
+      const double dz = exp(z[j] - mx) / Ls * (dp - Dr);
+      for (int32_t d = 0; d < d_qk; ++d) dqr[d] += scale * dz * (double)kj[d];
+    }
+    m[r] = mx;
+    L[r] = Ls;
+    D[r] = Dr;
+    free(mrow);
+    free(z);
+  }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t j = 0; j < n_kv; ++j) {
+    const float* kj = k + j * k_stride;
+    const float* vj = v + j * v_stride;
+    double* dkj = dk + j * d_qk;
+    double* dvj = dv + j * d_v;
+    for (int32_t d = 0; d < d_qk; ++d) dkj[d] = 0.0;
+    for (int32_t d = 0; d < d_v; ++d) dvj[d] = 0.0;
+    for (int64_t r = 0; r < R; ++r) {
+      if (!allowed(pos[r], j, s, l, b, sparse, causal)) continue;
+      const float* qr = q + r * q_stride;
+      const float* dor = dout + r * do_stride;
+      double acc = 0.0;
+      for (int32_t d = 0; d < d_qk; ++d) acc += (double)qr[d] * (double)kj[d];
+      const double P = exp(scale * acc - m[r]) / L[r];
+      double dp = 0.0;
+      for (int32_t d = 0; d < d_v; ++d) dp += (double)dor[d] * (double)vj[d];
+      const double dz = P * (dp - D[r]);
+      for (int32_t d = 0; d < d_qk; ++d) dkj[d] += scale * dz * (double)qr[d];
+      for (int32_t d = 0; d < d_v; ++d) dvj[d] += P * (double)dor[d];
+    }
+  }
+  free(m);
+  free(L);
+  free(D);
 }
 
 int loza_oracle_num_threads(void) {

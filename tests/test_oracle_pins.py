@@ -282,3 +282,60 @@ def test_blend_gradient_finite_difference_spec170():
         lp = float(np.dot(d.astype(np.float64), oracle.blend(o, op, a + eps)[0]))
         lm = float(np.dot(d.astype(np.float64), oracle.blend(o, op, a - eps)[0]))
         assert abs((lp - lm) / (2 * eps) - da) <= 1e-9 * np.abs(d.astype(np.float64) * (o - op)).sum()
+
+
+# ---------------------------------------------------------------- attention backward
+def _loss(q, pos, k, v, do, scale, pat, sparse=True, causal=True):
+    o, _ = oracle.attention_rows(q, pos, k, v, scale, *pat, sparse=sparse, causal=causal)
+    return float((o * do.astype(np.float64)).sum())
+
+
+@pytest.mark.parametrize("sparse", [True, False])
+def test_backward_finite_differences(sparse):
+    """Central differences of L = sum dO . O(Q, K, V) through the FORWARD oracle (independent of the backward
+    formulas) on random entries of q, k and v; h = 2^-10 is exact in fp32 for |x| < 2^13."""
+    rng = np.random.default_rng(7)
+    pat = (1, 2, 4)
+    R, n_kv, dqk, dv = 9, 20, 6, 5
+    pos = np.array([0, 3, 4, 7, 8, 12, 15, 18, 19], dtype=np.int64)
+    q = rng.standard_normal((R, dqk)).astype(np.float32)
+    k = rng.standard_normal((n_kv, dqk)).astype(np.float32)
+    v = rng.standard_normal((n_kv, dv)).astype(np.float32)
+    do = rng.standard_normal((R, dv)).astype(np.float32)
+    scale = 0.7
+    dq, dk, dvv = oracle.attention_backward(q, pos, k, v, do, scale, *pat, sparse=sparse)
+    h = 2.0 ** -10
+    for arr, grad in ((q, dq), (k, dk), (v, dvv)):
+        for idx in [tuple(rng.integers(0, d) for d in arr.shape) for _ in range(12)]:
+            xp, xm = arr.copy(), arr.copy()
+            xp[idx] += h
+            xm[idx] -= h
+            if arr is q:
+                lp, lm = _loss(xp, pos, k, v, do, scale, pat, sparse), _loss(xm, pos, k, v, do, scale, pat, sparse)
+            elif arr is k:
+                lp, lm = _loss(q, pos, xp, v, do, scale, pat, sparse), _loss(q, pos, xm, v, do, scale, pat, sparse)
+            else:
+                lp, lm = _loss(q, pos, k, xp, do, scale, pat, sparse), _loss(q, pos, k, xm, do, scale, pat, sparse)
+            fd = (lp - lm) / (2 * h)
+            assert abs(fd - grad[idx]) <= 1e-5 * max(1.0, abs(grad[idx])), (idx, fd, grad[idx])
+
+
+def test_backward_single_key_and_constant_v():
+    """One allowed key: P = 1, so dq = dk = 0 and dv = sum of dO over the rows. V rows all equal: O = v for any
+    P, so dq = dk = 0 and dv_j = sum_r P_rj dO_r (sums to sum dO over keys)."""
+    rng = np.random.default_rng(8)
+    R, dqk, dv = 5, 4, 3
+    q = rng.standard_normal((R, dqk)).astype(np.float32)
+    do = rng.standard_normal((R, dv)).astype(np.float32)
+    k1 = rng.standard_normal((1, dqk)).astype(np.float32)
+    v1 = rng.standard_normal((1, dv)).astype(np.float32)
+    dq, dk, dvv = oracle.attention_backward(q, np.zeros(R, dtype=np.int64), k1, v1, do, 0.5, 0, 1, 1, sparse=False)
+    assert np.abs(dq).max() < 1e-14 and np.abs(dk).max() < 1e-14
+    assert np.allclose(dvv[0], do.astype(np.float64).sum(0), rtol=0, atol=1e-12)
+    n_kv = 6
+    kc = rng.standard_normal((n_kv, dqk)).astype(np.float32)
+    vc = np.tile(rng.standard_normal((1, dv)).astype(np.float32), (n_kv, 1))
+    pos = np.full(R, n_kv - 1, dtype=np.int64)
+    dq, dk, dvv = oracle.attention_backward(q, pos, kc, vc, do, 0.5, 0, 1, 1, sparse=False)
+    assert np.abs(dq).max() < 1e-12 and np.abs(dk).max() < 1e-12
+    assert np.allclose(dvv.sum(0), do.astype(np.float64).sum(0), rtol=0, atol=1e-12)
