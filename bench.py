@@ -343,6 +343,18 @@ def extra_rows(args, q, kv, o, flush, peaks):
         "ssa_frac_tensor_in_fused": ssa_pairs(n8, *PATTERN) * FLOP_PER_PAIR / (fu_ms * 1e-3) / 1e12
         / peaks["bf16_tflops"],
         "note": "unfused = ssa_prefill (writes O') + loza_blend with d_alpha (reads O, O', dO_hat; writes O_hat)"}
+    # attention backward at the same 8K shape: SSA gradients of Q and the latent KV
+    lse8 = torch.empty((1, H, n8), device=dev)
+    loza.ssa_prefill(q8, kv8, pattern=PATTERN, scale=scale, out=osp, lse=lse8)
+    t_bw = _time_events(lambda: loza.attention_backward(q8, kv8, osp, lse8, dh, pattern=PATTERN, scale=scale),
+                        1, 1, flush)  # ~6 s per call in the FFMA first version
+    bw_ms = float(np.mean(t_bw))
+    bw_flop = ssa_pairs(n8, *PATTERN) * H * 2 * (3 * D_QK + 2 * D_V)  # recompute S, dP, dQ, dK, dV
+    out["backward_ssa_8k"] = {
+        "ms": bw_ms, "tflops": bw_flop / (bw_ms * 1e-3) / 1e12,
+        "frac_tensor": bw_flop / (bw_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+        "kernel": "FFMA first version (attn_bwd_simt.cu): correctness path, tensor-core version next",
+        "algorithmic_flop": bw_flop}
     del of, osp, dh, oh
     # decode B64 at 128K / 512K / 1M (configs[3])
     if not args.no_decode:

@@ -137,6 +137,21 @@ loza_status_t ssa_prefill_blend(const loza_attn_args_t* args, loza_pattern_t pat
                                 const float* alpha_dev, const void* d_o_hat, double* d_alpha_dev,
                                 int32_t* status_dev, void* ws, size_t ws_bytes, loza_stream_t stream);
 
+/* Attention backward: the gradients of Eq. 4 (sparse = 1, `pattern`) or Eq. 1 (sparse = 0,
+ * args->causal) for a loss with dL/dO = d_o. args describes the FORWARD call (q, k, v, o, softmax_scale,
+ * q_start, layouts as in ssa_prefill) and args->lse (the forward's LSE [B, H, n_q], natural log) is required;
+ * d_o has o's dtype and layout. Outputs (fp32, contiguous):
+ *   d_q [B, n_q, H, d_qk] = scale * sum_j dS_rj k_j,    dS_rj = P_rj (d_o_r . v_j - d_o_r . o_r)
+ *   d_k [B, n_kv, d_qk]   = scale * sum_r dS_rj q_r,    P_rj  = exp(scale q_r . k_j - lse_r)
+ *   d_v [B, n_kv, d_v]    = sum_r P_rj d_o_r
+ * summed over every query row (all heads) that attends the key. For the absorbed MLA cache (v = the first
+ * d_v columns of k) the cache gradient is d_k + [d_v, 0]. First GPU path: FFMA, fp32 accumulation,
+ * deterministic (no atomics); d_qk <= 576, d_v <= 512 (else LOZA_ERR_UNSUPPORTED).
+ * ws: loza_workspace_size(LOZA_WS_BACKWARD, args, pattern, 1) bytes. */
+loza_status_t attention_backward(const loza_attn_args_t* args, int32_t sparse, loza_pattern_t pattern,
+                                 const void* d_o, float* d_q, float* d_k, float* d_v, void* ws, size_t ws_bytes,
+                                 loza_stream_t stream);
+
 /* Bounded SSA KV cache. Per sequence R = (s+l)*b rows:
  * the s sink blocks at rows [0, s*b) and a ring of l blocks, block kb >= s at rows
  * s*b + ((kb - s) mod l)*b. Appending in position order evicts a local block exactly when it can no longer
@@ -193,7 +208,7 @@ loza_status_t loza_seqpar_prefill_local(const loza_attn_args_t* args, loza_patte
 loza_status_t ssa_select_blocks(int64_t n_q, int64_t q_start, loza_pattern_t pattern, int32_t causal,
                                 int32_t* idx_dev, int32_t* count_dev, loza_stream_t stream);
 
-enum { LOZA_WS_DECODE = 0, LOZA_WS_FULL_DECODE = 1, LOZA_WS_BLEND = 2, LOZA_WS_SEQPAR = 3 };
+enum { LOZA_WS_DECODE = 0, LOZA_WS_FULL_DECODE = 1, LOZA_WS_BLEND = 2, LOZA_WS_SEQPAR = 3, LOZA_WS_BACKWARD = 4 };
 /* Workspace bytes for `which`; args may be NULL for LOZA_WS_BLEND. */
 size_t loza_workspace_size(int32_t which, const loza_attn_args_t* args, loza_pattern_t pattern, int32_t world);
 

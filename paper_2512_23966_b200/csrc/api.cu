@@ -215,6 +215,24 @@ loza_status_t ssa_prefill_blend(const loza_attn_args_t* args, loza_pattern_t pat
   return cuda_status(launch_prefill_tc(p, (cudaStream_t)stream), "prefill_tc (calibration) launch");
 }
 
+loza_status_t attention_backward(const loza_attn_args_t* args, int32_t sparse, loza_pattern_t pattern,
+                                 const void* d_o, float* d_q, float* d_k, float* d_v, void* ws, size_t ws_bytes,
+                                 loza_stream_t stream) {
+  g_last_error[0] = 0;
+  if (sparse != 0 && sparse != 1) return fail(LOZA_ERR_INVALID, "sparse must be 0 or 1");
+  AttnProblem p;
+  loza_pattern_t none = {0, 1, 1};
+  loza_status_t rc = make_problem(args, sparse != 0, sparse ? pattern : none, nullptr, &p);
+  if (rc != LOZA_OK) return rc;
+  if (!args->lse) return fail(LOZA_ERR_INVALID, "attention_backward needs the forward's lse");
+  if (!d_o || !d_q || !d_k || !d_v) return fail(LOZA_ERR_INVALID, "NULL gradient pointer");
+  if (args->d_qk > 576 || args->d_v > 512) return fail(LOZA_ERR_UNSUPPORTED, "d_qk <= 576 and d_v <= 512");
+  if ((int64_t)p.batch * (p.n_q * (int64_t)p.heads + p.n_kv) == 0) return LOZA_OK;
+  const size_t need = backward_ws_bytes(p);
+  if (need > 0 && (!ws || ws_bytes < need)) return fail(LOZA_ERR_INVALID, "workspace too small (%zu < %zu)", ws_bytes, need);
+  return cuda_status(launch_attn_backward(p, d_o, d_q, d_k, d_v, ws, (cudaStream_t)stream), "backward launch");
+}
+
 loza_status_t ssa_ring_append(const void* rows, int64_t rows_stride_b, int64_t rows_stride_tok, int32_t m,
                               const int32_t* pos0_dev, loza_pattern_t pat, void* cache, int64_t cache_stride_b,
                               int64_t cache_stride_tok, int32_t batch, int32_t d, loza_dtype_t dtype,
@@ -274,6 +292,11 @@ size_t loza_workspace_size(int32_t which, const loza_attn_args_t* a, loza_patter
   if (which == LOZA_WS_BLEND) return blend_ws_bytes();
   if (!a) return 0;
   AttnProblem p;
+  if (which == LOZA_WS_BACKWARD) {
+    if (make_problem(a, pat.local_blocks >= 1 && pat.block_size >= 1 && a->causal, pat, nullptr, &p) != LOZA_OK)
+      return 0;
+    return backward_ws_bytes(p);
+  }
   if (which == LOZA_WS_DECODE || which == LOZA_WS_FULL_DECODE) {
     static const int32_t dummy = 1;
     if (make_problem(a, which == LOZA_WS_DECODE, pat, &dummy, &p) != LOZA_OK) return 0;

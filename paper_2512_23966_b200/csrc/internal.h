@@ -67,6 +67,9 @@ cudaError_t launch_decode_tc(const AttnProblem& p, void* ws, size_t ws_bytes, cu
 size_t decode_tc_ws_bytes(const AttnProblem& p);
 bool decode_pair_eligible(const AttnProblem& a, int sms);
 cudaError_t launch_decode_pair(const AttnProblem& a, cudaStream_t st);
+size_t backward_ws_bytes(const AttnProblem& a);
+cudaError_t launch_attn_backward(const AttnProblem& a, const void* dout, float* dq, float* dk, float* dv, void* ws,
+                                 cudaStream_t st);
 cudaError_t launch_ring_append(const void* rows, int64_t r_sb, int64_t r_st, int32_t m, const int32_t* pos0,
                                int32_t s, int32_t l, int32_t b, void* cache, int64_t c_sb, int64_t c_st,
                                int32_t batch, int32_t row_bytes, cudaStream_t st);

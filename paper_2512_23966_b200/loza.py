@@ -18,12 +18,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LOZA_LIB") or os.path.join(_HERE, "libloza.so")
 
 LOZA_F32, LOZA_BF16 = 0, 1
-LOZA_WS_DECODE, LOZA_WS_FULL_DECODE, LOZA_WS_BLEND, LOZA_WS_SEQPAR = 0, 1, 2, 3
+LOZA_WS_DECODE, LOZA_WS_FULL_DECODE, LOZA_WS_BLEND, LOZA_WS_SEQPAR, LOZA_WS_BACKWARD = 0, 1, 2, 3, 4
 STATUS = {0: "LOZA_OK", 1: "LOZA_ERR_INVALID", 2: "LOZA_ERR_SHAPE", 3: "LOZA_ERR_UNSUPPORTED",
           4: "LOZA_ERR_CUDA", 5: "LOZA_ERR_NCCL"}
 
 PAPER_PATTERN = (1, 7, 128)  # (s, l, b)
-EXPORTS = ["ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_prefill_blend", "ssa_ring_append",
+EXPORTS = ["ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_prefill_blend", "attention_backward",
+           "ssa_ring_append",
            "ssa_decode_ring", "ssa_seqpar_prefill",
            "loza_seqpar_prefill_local", "ssa_select_blocks", "loza_workspace_size", "loza_status_string",
            "loza_last_error", "loza_kernel_launches", "loza_num_sms"]
@@ -70,6 +71,7 @@ def lib():
         L.loza_blend.argtypes = [V, V, V, V, V, V, I64, S, V, V, SZ, V]
         L.ssa_prefill_blend.argtypes = [P(AttnArgs), Pattern, V, V, V, V, V, V, SZ, V]
         L.ssa_ring_append.argtypes = [V, I64, I64, I32, V, Pattern, V, I64, I64, I32, I32, S, V]
+        L.attention_backward.argtypes = [P(AttnArgs), I32, Pattern, V, V, V, V, V, SZ, V]
         L.ssa_decode_ring.argtypes = [P(AttnArgs), V, Pattern, V]
         L.ssa_seqpar_prefill.argtypes = [P(AttnArgs), Pattern, V, I32, I32, V, SZ, V]
         L.loza_seqpar_prefill_local.argtypes = [P(AttnArgs), Pattern, I32, I32, V, V, V, V, V, SZ, V]
@@ -204,6 +206,35 @@ def ssa_prefill_blend(q, k, o_full, alpha, d_o_hat=None, v=None, pattern=PAPER_P
                                    V(status.data_ptr() if status is not None else 0), V(ws.data_ptr()), need,
                                    _stream(stream)))
     return o, d_alpha
+
+
+def attention_backward(q, k, o, lse, d_o, v=None, pattern=PAPER_PATTERN, scale=None, *, d_v=512, causal=True,
+                       q_start=0, stream=None):
+    """Gradients of SSA (pattern) or full attention (pattern=None) for dL/dO = d_o, given the forward's
+    q, k (v: default MLA slice of k), o and lse [B,H,n_q]. Returns fp32 (d_q [B,n_q,H,dqk], d_k [B,n_kv,dqk],
+    d_v [B,n_kv,dv]); for the MLA cache the gradient is d_k + [d_v, 0]."""
+    k, v = _split_kv(k, v, d_v)
+    scale = default_scale(q.shape[-1]) if scale is None else scale
+    a = make_args(q, k, v, o, scale=scale, causal=causal, q_start=q_start, lse=lse)
+    o4 = _q4(o)
+    if d_o.dtype != o.dtype or d_o.numel() != o4.numel():
+        raise ValueError(f"d_o must match o (dtype {o.dtype}, {tuple(o4.shape)}); got {d_o.dtype}, {tuple(d_o.shape)}")
+    do4 = d_o.reshape(o4.shape)
+    if do4.stride() != o4.stride():
+        raise ValueError(f"d_o must have o's layout: strides {o4.stride()} vs {do4.stride()}")
+    B, n_q, H, dqk = _q4(q).shape
+    n_kv, dv = _kv3(k).shape[1], v.shape[-1]
+    dq = torch.empty((B, n_q, H, dqk), dtype=torch.float32, device=q.device)
+    dk = torch.empty((B, n_kv, dqk), dtype=torch.float32, device=q.device)
+    dvv = torch.empty((B, n_kv, dv), dtype=torch.float32, device=q.device)
+    pat = pattern if pattern is not None else (0, 1, 1)
+    need = lib().loza_workspace_size(LOZA_WS_BACKWARD, ctypes.byref(a), _pattern(pat), 1)
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device=q.device)
+    V = ctypes.c_void_p
+    _check(lib().attention_backward(ctypes.byref(a), 1 if pattern is not None else 0, _pattern(pat),
+                                    V(do4.data_ptr()), V(dq.data_ptr()), V(dk.data_ptr()), V(dvv.data_ptr()),
+                                    V(ws.data_ptr()), need, _stream(stream)))
+    return dq, dk, dvv
 
 
 def ring_rows(pattern=PAPER_PATTERN) -> int:

@@ -1,0 +1,99 @@
+"""GPU parity of attention_backward against the fp64 oracle backward (itself pinned by
+finite differences of the forward oracle, tests/test_oracle_pins.py).
+
+Tolerances (R12): fp32 inputs normwise ||d||_inf / ||ref||_inf <= 1e-4; bf16 MLA <= 2e-2 (the
+forward's O, used for D = dO . O, is bf16-rounded: ~2^-9 relative, and P is recomputed from the forward LSE).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from inputs import TID_DO, TID_K, TID_Q, TID_V, Spec, gen_rows_f32
+from inputs.device import empty_filled
+from paper_2512_23966_b200 import loza
+
+pytestmark = pytest.mark.gpu
+
+
+def _norm_err(got, ref):
+    return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+@pytest.mark.parametrize("sparse", [True, False])
+def test_backward_tiny_fp32(sparse):
+    """configs[0] shape (H=1, d=64, separate K/V, fp32), all rows and keys."""
+    B, n, H, d = 1, 512, 1, 64
+    pat = (1, 2, 64)
+    qs = Spec(seed=41, tensor_id=TID_Q, batch=B, n=n, heads=H, d=d, dtype="f32")
+    ks = Spec(seed=41, tensor_id=TID_K, batch=B, n=n, heads=1, d=d, dtype="f32")
+    vs = Spec(seed=41, tensor_id=TID_V, batch=B, n=n, heads=1, d=d, dtype="f32")
+    ds = Spec(seed=41, tensor_id=TID_DO, batch=B, n=n, heads=H, d=d, dtype="f32")
+    q, k, v, do = (empty_filled(s) for s in (qs, ks, vs, ds))
+    scale = 0.125
+    lse = torch.empty((B, H, n), device="cuda")
+    if sparse:
+        o = loza.ssa_prefill(q, k, v, pat, scale, d_v=d, lse=lse)
+    else:
+        o = loza.full_attn_ref(q, k, v, scale, d_v=d, lse=lse)
+    dq, dk, dv = loza.attention_backward(q, k, o, lse, do, v=v, pattern=pat if sparse else None, scale=scale, d_v=d)
+    torch.cuda.synchronize()
+    rq, rk, rv = oracle.attention_backward(gen_rows_f32(qs, 0, n), np.arange(n), gen_rows_f32(ks, 0, n),
+                                           gen_rows_f32(vs, 0, n), gen_rows_f32(ds, 0, n), scale, *pat,
+                                           sparse=sparse)
+    assert _norm_err(dq[0, :, 0].double().cpu().numpy(), rq) <= 1e-4
+    assert _norm_err(dk[0].double().cpu().numpy(), rk) <= 1e-4
+    assert _norm_err(dv[0].double().cpu().numpy(), rv) <= 1e-4
+
+
+def test_backward_mla_bf16_ssa():
+    """absorbed MLA shape (576/512, H=64, V = KV[:, :512]), bf16, (1,1,128) over n = 256 (a sink-only and a
+    sink+local query block), every row and key; MLA cache gradient d_kv = d_k + [d_v, 0]."""
+    B, n, H = 1, 256, 64
+    pat = (1, 1, 128)
+    qs = Spec(seed=42, tensor_id=TID_Q, batch=B, n=n, heads=H, d=576)
+    ks = Spec(seed=42, tensor_id=TID_K, batch=B, n=n, heads=1, d=576)
+    ds = Spec(seed=42, tensor_id=TID_DO, batch=B, n=n, heads=H, d=512)
+    q, kv, do = empty_filled(qs), empty_filled(ks), empty_filled(ds)
+    scale = loza.default_scale(576)
+    lse = torch.empty((B, H, n), device="cuda")
+    o = loza.ssa_prefill(q, kv, pattern=pat, scale=scale, lse=lse)
+    dq, dk, dv = loza.attention_backward(q, kv, o, lse, do, pattern=pat, scale=scale)
+    dq2, dk2, dv2 = loza.attention_backward(q, kv, o, lse, do, pattern=pat, scale=scale)
+    torch.cuda.synchronize()
+    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)  # deterministic
+    kf = gen_rows_f32(ks, 0, n)
+    rq, rk, rv = oracle.attention_backward(gen_rows_f32(qs, 0, n * H), np.repeat(np.arange(n), H), kf, kf[:, :512],
+                                           gen_rows_f32(ds, 0, n * H), scale, *pat)
+    assert _norm_err(dq[0].reshape(n * H, 576).double().cpu().numpy(), rq) <= 2e-2
+    assert _norm_err(dk[0].double().cpu().numpy(), rk) <= 2e-2
+    assert _norm_err(dv[0].double().cpu().numpy(), rv) <= 2e-2
+    # MLA: the cache gradient composes d_k and d_v
+    dkv = dk.clone()
+    dkv[..., :512] += dv
+    rkv = rk.copy()
+    rkv[:, :512] += rv
+    assert _norm_err(dkv[0].double().cpu().numpy(), rkv) <= 2e-2
+
+
+def test_backward_q_start_offset():
+    """queries [q_start, n) against keys [0, n) (chunked prefill), fp32 tiny dims, SSA."""
+    B, n, H, d, q0 = 1, 384, 2, 32, 128
+    pat = (1, 2, 64)
+    qs = Spec(seed=43, tensor_id=TID_Q, batch=B, n=n, heads=H, d=d, dtype="f32")
+    ks = Spec(seed=43, tensor_id=TID_K, batch=B, n=n, heads=1, d=d, dtype="f32")
+    ds = Spec(seed=43, tensor_id=TID_DO, batch=B, n=n, heads=H, d=d, dtype="f32")
+    q, kv, do = empty_filled(qs), empty_filled(ks), empty_filled(ds)
+    scale = 0.2
+    lse = torch.empty((B, H, n - q0), device="cuda")
+    qq = q[:, q0:].contiguous()
+    dd = do[:, q0:].contiguous()
+    o = loza.ssa_prefill(qq, kv, kv, pat, scale, d_v=d, q_start=q0, lse=lse)
+    dq, dk, dv = loza.attention_backward(qq, kv, o, lse, dd, v=kv, pattern=pat, scale=scale, d_v=d, q_start=q0)
+    torch.cuda.synchronize()
+    kf = gen_rows_f32(ks, 0, n)
+    rq, rk, rv = oracle.attention_backward(gen_rows_f32(qs, q0 * H, (n - q0) * H), np.repeat(np.arange(q0, n), H),
+                                           kf, kf, gen_rows_f32(ds, q0 * H, (n - q0) * H), scale, *pat)
+    assert _norm_err(dq[0].reshape(-1, d).double().cpu().numpy(), rq) <= 1e-4
+    assert _norm_err(dk[0].double().cpu().numpy(), rk) <= 1e-4
+    assert _norm_err(dv[0].double().cpu().numpy(), rv) <= 1e-4
