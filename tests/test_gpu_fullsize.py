@@ -1,0 +1,106 @@
+"""Parity at the BASELINE.json sizes the bench times, on sampled outputs the fp64 oracle computes one by one
+(DESIGN.md §3): blend and the fused calibration forward at 8K (configs[2]), the ring-cache decode at position
+1M (configs[3]), and the sequence-parallel prefill at 8 virtual ranks (the bench's largest topology).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from inputs import TID_DO, TID_K, TID_O_FULL, TID_O_SPARSE, TID_Q, Spec, gen_rows_f32
+from inputs.device import empty_filled
+from paper_2512_23966_b200 import loza
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+H, D_QK, D_V = 64, 576, 512
+PAT = (1, 7, 128)
+
+
+def test_blend_8k_sampled():
+    n = 8192
+    mk = lambda tid: Spec(seed=51, tensor_id=tid, batch=1, n=n, heads=H, d=D_V)  # noqa: E731
+    of, os_, dh = (empty_filled(mk(t)) for t in (TID_O_FULL, TID_O_SPARSE, TID_DO))
+    a = torch.tensor([0.3], dtype=torch.float32, device="cuda")
+    oh, da = loza.loza_blend(of.view(-1), os_.view(-1), a, dh.view(-1))
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    rows = rng.integers(0, n * H, 64)
+    for r in rows:
+        f = [gen_rows_f32(mk(t), int(r), 1)[0] for t in (TID_O_FULL, TID_O_SPARSE)]
+        rh, _ = oracle.blend(f[0], f[1], 0.3)
+        got = oh.view(n * H, D_V)[int(r)].double().cpu().numpy()
+        assert np.abs(got - rh).max() <= 2.0 ** -8 * np.abs(rh).max() + 1e-6
+    # d_alpha over the whole 268M elements against the fp64 sum on the same bits (chunked on the host)
+    ref, mag = 0.0, 0.0
+    for c in range(0, n, 512):
+        f = [x[0, c:c + 512].double().cpu().numpy().ravel() for x in (of, os_, dh)]
+        ref += float((f[2] * (f[0] - f[1])).sum())
+        mag += float(np.abs(f[2] * (f[0] - f[1])).sum())
+    assert abs(float(da.item()) - ref) <= 1e-4 * mag
+
+
+def test_calibration_fused_8k_sampled():
+    n = 8192
+    qs = Spec(seed=52, tensor_id=TID_Q, batch=1, n=n, heads=H, d=D_QK)
+    ks = Spec(seed=52, tensor_id=TID_K, batch=1, n=n, heads=1, d=D_QK)
+    ofs = Spec(seed=52, tensor_id=TID_O_FULL, batch=1, n=n, heads=H, d=D_V)
+    q, kv, of = empty_filled(qs), empty_filled(ks), empty_filled(ofs)
+    a = torch.tensor([0.6], dtype=torch.float32, device="cuda")
+    oh, _ = loza.ssa_prefill_blend(q, kv, of, a, pattern=PAT)
+    torch.cuda.synchronize()
+    kf = gen_rows_f32(ks, 0, n)
+    scale = loza.default_scale(D_QK)
+    for t in [0, 1023, 1024, 4097, 8191]:
+        qr = gen_rows_f32(qs, t * H, H)
+        osp, _ = oracle.attention_rows(qr, np.full(H, t), kf, kf[:, :D_V], scale, *PAT)
+        rh, _ = oracle.blend(gen_rows_f32(ofs, t * H, H), osp, 0.6)
+        assert np.abs(oh[0, t].double().cpu().numpy().ravel() - rh).max() <= 2e-2, t
+
+
+def test_ring_decode_at_1m_sampled():
+    """B = 8 sequences at absolute position 1,048,576 - 1 - j, ring caches filled from the windows'
+    rows; rows against the oracle over the same window (sink block + 7 local blocks)."""
+    B, T = 8, 1 << 20
+    s, l, b = PAT
+    ks = Spec(seed=53, tensor_id=TID_K, batch=B, n=T, heads=1, d=D_QK)
+    qs = Spec(seed=53, tensor_id=TID_Q, batch=B, n=1, heads=H, d=D_QK)
+    q = empty_filled(qs)
+    lens = [T - 7 * j for j in range(B)]
+    cache = torch.zeros((B, (s + l) * b, D_QK), dtype=torch.bfloat16, device="cuda")
+    for bi, L in enumerate(lens):
+        # only the rows the window of position L-1 needs: the sink block and the last l blocks
+        qb = (L - 1) // b
+        starts = [0] + [k * b for k in range(max(s, qb - l + 1), qb + 1)]
+        for st in starts:
+            rows = torch.from_numpy(gen_rows_f32(ks, bi * T + st, min(b, L - st))).to("cuda").to(torch.bfloat16)
+            loza.ssa_ring_append(cache[bi:bi + 1], rows.unsqueeze(0),
+                                 torch.tensor([st], dtype=torch.int32, device="cuda"), pattern=PAT)
+    seq = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    o = loza.ssa_decode_ring(q, cache, seq, pattern=PAT)
+    torch.cuda.synchronize()
+    scale = loza.default_scale(D_QK)
+    for bi, L in enumerate(lens):
+        keys = oracle.allowed_keys(L - 1, L, s, l, b)
+        kf = np.stack([gen_rows_f32(ks, bi * T + int(j), 1)[0] for j in keys])
+        qr = gen_rows_f32(qs, bi * H, H)
+        ref, _ = oracle.attend(qr, kf, kf[:, :D_V], scale)
+        assert np.abs(o[bi, 0].double().cpu().numpy() - ref).max() <= 2e-2, bi
+
+
+def test_seqpar_8_virtual_ranks_bitwise():
+    """8 ranks x 4096 tokens (32K total, MLA bf16, (1,7,128)): every shard through the exchange-then-SSA path
+    equals the single-GPU prefill bitwise."""
+    world, n_local = 8, 4096
+    n = world * n_local
+    qs = Spec(seed=54, tensor_id=TID_Q, batch=1, n=n, heads=H, d=D_QK)
+    ks = Spec(seed=54, tensor_id=TID_K, batch=1, n=n, heads=1, d=D_QK)
+    q, kv = empty_filled(qs), empty_filled(ks)
+    ref = loza.ssa_prefill(q, kv, pattern=PAT)
+    shards = [kv[:, r * n_local:(r + 1) * n_local].contiguous() for r in range(world)]
+    for r in range(world):
+        o = loza.ssa_seqpar_prefill_local(q[:, r * n_local:(r + 1) * n_local].contiguous(), shards[r], None, PAT,
+                                          loza.default_scale(D_QK), rank=r, world=world, rank0_k=shards[0],
+                                          prev_k=shards[r - 1] if r > 0 else None)
+        torch.cuda.synchronize()
+        assert torch.equal(o, ref[:, r * n_local:(r + 1) * n_local]), r
