@@ -241,15 +241,41 @@ def run_gpu(args):
         qd = torch.empty_like(q)
         kd = torch.empty_like(kv)
 
+        # Chunked prefill through the public API (q_start = chunk offset, KV prefix up to the chunk's end):
+        # chunk c's upload, chunk c-1's SSA and chunk c-2's download overlap on three streams (PCIe is full
+        # duplex), all inside the events the timing helper records on the calling stream. Units are
+        # independent, so the output equals the unchunked prefill bit for bit.
+        n_chunks = 16
+        nc = n_local // n_chunks
+        s_h, s_c, s_d = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        ev_h = [torch.cuda.Event() for _ in range(n_chunks)]
+        ev_c = [torch.cuda.Event() for _ in range(n_chunks)]
+
         def e2e_step():
-            qd.copy_(qh, non_blocking=True)
-            kd.copy_(kh, non_blocking=True)
-            loza.ssa_prefill(qd, kd, pattern=PATTERN, scale=scale, out=o)
-            oh.copy_(o, non_blocking=True)
+            cur = torch.cuda.current_stream()
+            s_h.wait_stream(cur)
+            s_c.wait_stream(cur)
+            s_d.wait_stream(cur)
+            for c in range(n_chunks):
+                a, e = c * nc, (c + 1) * nc
+                with torch.cuda.stream(s_h):
+                    qd[:, a:e].copy_(qh[:, a:e], non_blocking=True)
+                    kd[:, a:e].copy_(kh[:, a:e], non_blocking=True)
+                    ev_h[c].record(s_h)
+                s_c.wait_event(ev_h[c])
+                with torch.cuda.stream(s_c):
+                    loza.ssa_prefill(qd[:, a:e], kd[:, :e], pattern=PATTERN, scale=scale, out=o[:, a:e], q_start=a)
+                    ev_c[c].record(s_c)
+                s_d.wait_event(ev_c[c])
+                with torch.cuda.stream(s_d):
+                    oh[:, a:e].copy_(o[:, a:e], non_blocking=True)
+            cur.wait_stream(s_d)
+            cur.wait_stream(s_c)
         ts = _time_events(e2e_step, max(2, args.steps // 2), 1)
         e2e = {"value": n_local / (float(np.mean(ts)) * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(q.numel() * 2 + kv.numel() * 2), "d2h_bytes_per_step": int(o.numel() * 2),
-               "ms_per_step": float(np.mean(ts))}
+               "ms_per_step": float(np.mean(ts)),
+               "method": f"ssa_prefill in {n_chunks} chunks (q_start), H2D / compute / D2H on three streams"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

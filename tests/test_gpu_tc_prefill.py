@@ -162,3 +162,17 @@ def test_seqpar_local_emulation_bf16_mla_bitwise(world):
                                           prev_k=shards[r - 1] if r > 0 else None)
         torch.cuda.synchronize()
         assert torch.equal(o, ref[:, r * n_local:(r + 1) * n_local]), r
+
+
+def test_chunked_prefill_bitwise():
+    """chunked prefill through q_start (queries [a, e) against the KV prefix [0, e)) equals the whole-sequence
+    prefill bit for bit (work units are independent); this is how bench.py's e2e leg pipelines PCIe."""
+    n, H, pat, nc = 4096, 64, (1, 7, 128), 1024
+    qs, ks = _specs(8, 1, n, H)
+    q, kv = empty_filled(qs), empty_filled(ks)
+    ref = loza.ssa_prefill(q, kv, pattern=pat, scale=SCALE)
+    out = torch.empty_like(ref)
+    for a in range(0, n, nc):
+        loza.ssa_prefill(q[:, a:a + nc], kv[:, :a + nc], pattern=pat, scale=SCALE, out=out[:, a:a + nc], q_start=a)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
