@@ -382,6 +382,12 @@ def extra_rows(args, q, kv, o, flush, peaks):
         "kernel": "FFMA first version (attn_bwd_simt.cu): correctness path, tensor-core version next",
         "algorithmic_flop": bw_flop}
     del of, osp, dh, oh
+    if not args.no_cpu:
+        try:
+            ot = oracle_row_timings()
+            out["oracle_beside_rows"] = ot
+        except Exception as e:  # noqa: BLE001
+            out["oracle_beside_rows"] = {"error": repr(e)[:200]}
     # decode B64 at 128K / 512K / 1M (configs[3])
     if not args.no_decode:
         try:
@@ -512,6 +518,48 @@ def cpu_baseline(seconds: float = 15.0):
             "sample": f"{done} random query tokens x 64 heads of the 32K SSA prefill (fp64, OpenMP over rows); "
                       f"{spent:.1f} s of oracle time ({wall:.1f} s wall incl. input regeneration)",
             "cpu_model": _cpu_model()}
+
+
+def oracle_row_timings(seconds_each: float = 1.5):
+    """The fp64 oracle timed beside the extra rows, each on a bounded sample extrapolated to the row's
+    workload (host cores, OpenMP). Returns {row: {...}}."""
+    import oracle
+    from inputs import TID_DO, TID_K, TID_Q, Spec, gen_rows_f32
+    out = {}
+    scale = loza_scale()
+    ks = Spec(seed=0, tensor_id=TID_K, batch=1, n=2048, heads=1, d=D_QK)
+    qs = Spec(seed=0, tensor_id=TID_Q, batch=1, n=2048, heads=H, d=D_QK)
+    kf = gen_rows_f32(ks, 0, 2048)
+    # decode: one sequence's step = 64 heads over the 1,024-key window
+    win = kf[:1024]
+    qr = gen_rows_f32(qs, 0, H)
+    n_it, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds_each:
+        oracle.attend(qr, win, np.ascontiguousarray(win[:, :D_V]), scale)
+        n_it += 1
+    per_seq = (time.perf_counter() - t0) / n_it
+    out["decode"] = {"oracle_ms_per_step_b64": per_seq * 64 * 1e3, "sample": f"{n_it} sequences (64 heads x 1024 keys)"}
+    # blend: elements per second
+    x = np.random.default_rng(0).standard_normal(1 << 22).astype(np.float32)
+    n_it, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds_each:
+        oracle.blend(x, x, 0.5, x)
+        n_it += 1
+    el_s = n_it * x.size / (time.perf_counter() - t0)
+    out["blend_8k"] = {"oracle_ms": 8192 * H * D_V / el_s * 1e3, "sample": f"{n_it} x 4M elements (Eq. 3 + d_alpha)"}
+    # backward: (row, key) pairs per second on a 256-token SSA problem, extrapolated to the 8K row
+    n_b = 256
+    qb = gen_rows_f32(qs, 0, n_b * H)
+    dos = Spec(seed=0, tensor_id=TID_DO, batch=1, n=n_b, heads=H, d=D_V)
+    dob = gen_rows_f32(dos, 0, n_b * H)
+    pos = np.repeat(np.arange(n_b), H)
+    t0 = time.perf_counter()
+    oracle.attention_backward(qb, pos, kf[:n_b], np.ascontiguousarray(kf[:n_b, :D_V]), dob, scale, *PATTERN)
+    dt = time.perf_counter() - t0
+    pairs_small = sum(min(t + 1, 1024) for t in range(n_b)) * H  # (1,7,128) window covers all of 256 tokens
+    out["backward_ssa_8k"] = {"oracle_ms": dt / pairs_small * ssa_pairs(8192, *PATTERN) * H * 1e3,
+                              "sample": f"{n_b} tokens x 64 heads, full backward (two passes)"}
+    return out
 
 
 def loza_scale():
