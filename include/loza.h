@@ -152,6 +152,18 @@ loza_status_t attention_backward(const loza_attn_args_t* args, int32_t sparse, l
                                  const void* d_o, float* d_q, float* d_k, float* d_v, void* ws, size_t ws_bytes,
                                  loza_stream_t stream);
 
+/* SSA prefill in the non-absorbed (MHA) form of MLA (Eq. 4, applied to the
+ * per-head keys/values an MLA layer produces when its latent window is up-projected). Each head
+ * h has its own K, V: q [B, n_q, H, 192] (128 nope + 64 RoPE dims), k [B, n_kv, H, 192], v [B, n_kv, H, 128],
+ * o [B, n_q, H, 128]; args->k_stride_b / k_stride_tok / v_* are the batch / token strides and
+ * k_stride_head / v_stride_head the head strides, all in elements (any layout whose innermost dimension is
+ * contiguous and whose strides are multiples of 16 bytes). Same selection as ssa_prefill (sparse = 1, b %
+ * 128 == 0) or, with sparse = 0, the full-attention comparator of Eq. 1 (causal, or bidirectional with
+ * q_start == 0). bf16 inputs; o bf16 (RN-even) or fp32; optional lse [B, H, n_q]. Returns
+ * LOZA_ERR_UNSUPPORTED for other head dims, LOZA_ERR_SHAPE for misaligned pointers/strides. */
+loza_status_t ssa_prefill_mha(const loza_attn_args_t* args, int64_t k_stride_head, int64_t v_stride_head,
+                              int32_t sparse, loza_pattern_t pattern, loza_stream_t stream);
+
 /* Bounded SSA KV cache. Per sequence R = (s+l)*b rows:
  * the s sink blocks at rows [0, s*b) and a ring of l blocks, block kb >= s at rows
  * s*b + ((kb - s) mod l)*b. Appending in position order evicts a local block exactly when it can no longer

@@ -233,6 +233,35 @@ loza_status_t attention_backward(const loza_attn_args_t* args, int32_t sparse, l
   return cuda_status(launch_attn_backward(p, d_o, d_q, d_k, d_v, ws, (cudaStream_t)stream), "backward launch");
 }
 
+loza_status_t ssa_prefill_mha(const loza_attn_args_t* args, int64_t k_stride_head, int64_t v_stride_head,
+                              int32_t sparse, loza_pattern_t pattern, loza_stream_t stream) {
+  g_last_error[0] = 0;
+  if (sparse != 0 && sparse != 1) return fail(LOZA_ERR_INVALID, "sparse must be 0 or 1");
+  AttnProblem p;
+  loza_pattern_t none = {0, 1, 1};
+  loza_status_t rc = make_problem(args, sparse != 0, sparse ? pattern : none, nullptr, &p);
+  if (rc != LOZA_OK) return rc;
+  if (args->d_qk != 192 || args->d_v != 128)
+    return fail(LOZA_ERR_UNSUPPORTED, "ssa_prefill_mha: per-head d_qk 192 (128 nope + 64 rope), d_v 128 only");
+  if (args->in_dtype != LOZA_BF16) return fail(LOZA_ERR_UNSUPPORTED, "ssa_prefill_mha: bf16 inputs only");
+  if (sparse && pattern.block_size % 128 != 0) return fail(LOZA_ERR_UNSUPPORTED, "ssa_prefill_mha needs b %% 128 == 0");
+  if (!sparse && !args->causal && args->q_start != 0)
+    return fail(LOZA_ERR_UNSUPPORTED, "bidirectional comparator needs q_start == 0");
+  if ((int64_t)p.batch * p.n_q * p.heads == 0) return LOZA_OK;
+  if (args->n_q > INT32_MAX / 2 || args->n_kv >= ((int64_t)1 << 31)) return fail(LOZA_ERR_SHAPE, "sizes too large");
+  const int64_t esz = 2, oesz = args->out_dtype == LOZA_BF16 ? 2 : 4;
+  if (!aligned16(args->q) || !aligned16(args->k) || !aligned16(args->v) || !aligned16(args->o))
+    return fail(LOZA_ERR_SHAPE, "ssa_prefill_mha needs 16-byte aligned base pointers");
+  const int64_t in_strides[] = {args->q_stride_b, args->q_stride_tok, args->q_stride_head, args->k_stride_b,
+                                args->k_stride_tok, k_stride_head, args->v_stride_b, args->v_stride_tok, v_stride_head};
+  for (int64_t s : in_strides)
+    if (s < 0 || (s * esz) % 16) return fail(LOZA_ERR_SHAPE, "ssa_prefill_mha needs 16-byte aligned, non-negative strides");
+  const int64_t o_strides[] = {args->o_stride_b, args->o_stride_tok, args->o_stride_head};
+  for (int64_t s : o_strides)
+    if (s < 0 || (s * oesz) % 16) return fail(LOZA_ERR_SHAPE, "ssa_prefill_mha needs 16-byte aligned output strides");
+  return cuda_status(launch_prefill_mha(p, k_stride_head, v_stride_head, (cudaStream_t)stream), "prefill_mha launch");
+}
+
 loza_status_t ssa_ring_append(const void* rows, int64_t rows_stride_b, int64_t rows_stride_tok, int32_t m,
                               const int32_t* pos0_dev, loza_pattern_t pat, void* cache, int64_t cache_stride_b,
                               int64_t cache_stride_tok, int32_t batch, int32_t d, loza_dtype_t dtype,

@@ -63,6 +63,8 @@ size_t blend_ws_bytes();
 cudaError_t launch_dalpha_reduce(const double* part, int n, const float* alpha, double* out, cudaStream_t st);
 // tcgen05 paths (bf16, d_qk 576, d_v 512)
 cudaError_t launch_prefill_tc(const AttnProblem& p, cudaStream_t st);
+// non-absorbed (MHA) form, d_qk 192 / d_v 128, per-head K/V (k_sh, v_sh: head strides in elements)
+cudaError_t launch_prefill_mha(const AttnProblem& a, int64_t k_sh, int64_t v_sh, cudaStream_t st);
 cudaError_t launch_decode_tc(const AttnProblem& p, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t decode_tc_ws_bytes(const AttnProblem& p);
 bool decode_pair_eligible(const AttnProblem& a, int sms);
@@ -90,6 +92,9 @@ namespace loza {
 // 3-D bf16 TMA map {d (contiguous), rows, batch}, box {64, box_rows, 1}, SWIZZLE_128B (tma_host.cu)
 bool encode_3d(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t batch, int64_t row_stride_el,
                int64_t batch_stride_el, uint32_t box_rows);
+bool encode_5d_heads(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t heads, uint64_t batch,
+                     int64_t row_stride_el, int64_t head_stride_el, int64_t batch_stride_el, uint32_t box_rows,
+                     uint32_t box_chunks);
 bool encode_4d_chunks(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t batch,
                       int64_t row_stride_el, int64_t batch_stride_el, uint32_t box_rows, uint32_t box_chunks);
 }  // namespace loza

@@ -57,4 +57,25 @@ bool encode_4d_chunks(CUtensorMap* m, const void* base, uint64_t d, uint64_t row
   return r == CUDA_SUCCESS;
 }
 
+// 5-D bf16 view of a per-head tensor [batch, rows, heads, d] (strides in elements): {64, rows, d/64 chunks,
+// heads, batch} with box {64, box_rows, box_chunks, 1, 1}: SMEM [chunk][row][64] (SWIZZLE_128B), i.e. the
+// layout of box_chunks separate [box_rows x 64] tiles, for one head.
+bool encode_5d_heads(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t heads, uint64_t batch,
+                     int64_t row_stride_el, int64_t head_stride_el, int64_t batch_stride_el, uint32_t box_rows,
+                     uint32_t box_chunks) {
+  auto enc = get_encode();
+  if (!enc || d % 64 != 0) return false;
+  if (rows == 0) rows = 1;
+  if (batch == 0) batch = 1;
+  cuuint64_t dims[5] = {64, rows, d / 64, heads, batch};
+  cuuint64_t strides[4] = {(cuuint64_t)row_stride_el * 2, 128, (cuuint64_t)head_stride_el * 2,
+                           (cuuint64_t)batch_stride_el * 2};
+  cuuint32_t box[5] = {64, box_rows, box_chunks, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace loza

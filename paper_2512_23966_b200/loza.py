@@ -24,7 +24,7 @@ STATUS = {0: "LOZA_OK", 1: "LOZA_ERR_INVALID", 2: "LOZA_ERR_SHAPE", 3: "LOZA_ERR
 
 PAPER_PATTERN = (1, 7, 128)  # (s, l, b)
 EXPORTS = ["ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_prefill_blend", "attention_backward",
-           "ssa_ring_append",
+           "ssa_prefill_mha", "ssa_ring_append",
            "ssa_decode_ring", "ssa_seqpar_prefill",
            "loza_seqpar_prefill_local", "ssa_select_blocks", "loza_workspace_size", "loza_status_string",
            "loza_last_error", "loza_kernel_launches", "loza_num_sms"]
@@ -73,6 +73,7 @@ def lib():
         L.ssa_ring_append.argtypes = [V, I64, I64, I32, V, Pattern, V, I64, I64, I32, I32, S, V]
         L.attention_backward.argtypes = [P(AttnArgs), I32, Pattern, V, V, V, V, V, SZ, V]
         L.ssa_decode_ring.argtypes = [P(AttnArgs), V, Pattern, V]
+        L.ssa_prefill_mha.argtypes = [P(AttnArgs), I64, I64, I32, Pattern, V]
         L.ssa_seqpar_prefill.argtypes = [P(AttnArgs), Pattern, V, I32, I32, V, SZ, V]
         L.loza_seqpar_prefill_local.argtypes = [P(AttnArgs), Pattern, I32, I32, V, V, V, V, V, SZ, V]
         L.ssa_select_blocks.argtypes = [I64, I64, Pattern, I32, V, V, V]
@@ -235,6 +236,33 @@ def attention_backward(q, k, o, lse, d_o, v=None, pattern=PAPER_PATTERN, scale=N
                                     V(do4.data_ptr()), V(dq.data_ptr()), V(dk.data_ptr()), V(dvv.data_ptr()),
                                     V(ws.data_ptr()), need, _stream(stream)))
     return dq, dk, dvv
+
+
+def ssa_prefill_mha(q, k, v, pattern=PAPER_PATTERN, scale=None, *, sparse=True, causal=True, out=None, lse=None,
+                    q_start=0, out_dtype=None, stream=None):
+    """Non-absorbed (MHA-form) SSA prefill: q [B,n_q,H,192], k [B,n_kv,H,192], v [B,n_kv,H,128]
+    (per-head K/V; any strides with a contiguous innermost dim). sparse=False: the full-attention comparator.
+    Returns O [B,n_q,H,128]."""
+    for t in (q, k, v):
+        if t.dim() != 4 or not t.is_cuda or t.stride(-1) != 1:
+            raise ValueError("q, k, v must be 4-D CUDA tensors [B, n, H, d] with a contiguous last dim")
+    B, n_q, H, dqk = q.shape
+    scale = 1.0 / math.sqrt(dqk) if scale is None else scale
+    o = out if out is not None else torch.empty((B, n_q, H, v.shape[-1]), dtype=out_dtype or q.dtype,
+                                                device=q.device)
+    a = AttnArgs()
+    a.batch, a.n_q, a.heads, a.d_qk, a.d_v = B, n_q, H, dqk, v.shape[-1]
+    a.n_kv, a.q_start = k.shape[1], q_start
+    a.in_dtype, a.out_dtype = _dt(q), _dt(o)
+    a.softmax_scale, a.causal = float(scale), 1 if causal else 0
+    a.q, a.q_stride_b, a.q_stride_tok, a.q_stride_head = q.data_ptr(), q.stride(0), q.stride(1), q.stride(2)
+    a.k, a.k_stride_b, a.k_stride_tok = k.data_ptr(), k.stride(0), k.stride(1)
+    a.v, a.v_stride_b, a.v_stride_tok = v.data_ptr(), v.stride(0), v.stride(1)
+    a.o, a.o_stride_b, a.o_stride_tok, a.o_stride_head = o.data_ptr(), o.stride(0), o.stride(1), o.stride(2)
+    a.lse = lse.data_ptr() if lse is not None else None
+    _check(lib().ssa_prefill_mha(ctypes.byref(a), k.stride(2), v.stride(2), 1 if sparse else 0, _pattern(pattern),
+                                 _stream(stream)))
+    return o
 
 
 def ring_rows(pattern=PAPER_PATTERN) -> int:
