@@ -208,6 +208,15 @@ __device__ __forceinline__ void umma_bf16_pair(uint32_t d_tmem, uint64_t a_desc,
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// A operand from TMEM (a_tmem: lane = row, K packed 2 bf16 per column, low half = lower k)
+__device__ __forceinline__ void umma_bf16_pair_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void umma_bf16_1sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                               uint32_t accumulate) {
   asm volatile(
@@ -283,6 +292,60 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
+}
+// ---- paired fp32 (FFMA2 / FADD2) and 3-input max (FMNMX3), sm_100
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2_rm(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// 2^x for a pair on the FMA pipe (x <= 127; x < -127 -> 0): floor via an add of 1.5 * 2^23 rounded toward
+// -inf, 2^frac by a degree-3 polynomial (max rel. error 8.8e-5, below bf16's 2^-9), exponent added as integer.
+// Offloads part of the softmax's exponentials from the 16/clk/SM MUFU.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  float x0, x1;
+  f2unpack(x, x0, x1);
+  const uint64_t xc = f2pack(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+  const uint64_t rnd = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t rd = fadd2_rm(xc, rnd);         // low mantissa bits = floor(x)
+  const uint64_t fr = fsub2(xc, fsub2(rd, rnd));  // x - floor(x) in [0, 1)
+  uint64_t p = ffma2(fr, f2pack(0.077119089663028717041015625f, 0.077119089663028717041015625f),
+                     f2pack(0.227564394474029541015625f, 0.227564394474029541015625f));
+  p = ffma2(p, fr, f2pack(0.695146143436431884765625f, 0.695146143436431884765625f));
+  p = ffma2(p, fr, f2pack(1.0f, 1.0f));
+  float r0, r1, p0, p1;
+  f2unpack(rd, r0, r1);
+  f2unpack(p, p0, p1);
+  return f2pack(__uint_as_float((__float_as_uint(r0) << 23) + __float_as_uint(p0)),
+                __uint_as_float((__float_as_uint(r1) << 23) + __float_as_uint(p1)));
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");

@@ -37,7 +37,8 @@ def _ref_head(specs, bi, h, rows, pat, scale, q_start=0, sparse=True, causal=Tru
     return oracle.attention_rows(qa, q_start + np.asarray(rows), ka, va, scale, *pat, sparse=sparse, causal=causal)
 
 
-@pytest.mark.parametrize("B,n,H,pat", [(2, 1000, 4, (1, 2, 128)), (1, 1536, 2, (2, 1, 256)), (1, 129, 3, (1, 7, 128))])
+@pytest.mark.parametrize("B,n,H,pat", [(2, 1000, 4, (1, 2, 128)), (1, 1536, 2, (2, 1, 256)), (1, 129, 3, (1, 7, 128)),
+                                      (1, 900, 2, (0, 2, 128)), (1, 1200, 2, (1, 2, 384))])
 def test_mha_ssa_all_rows(B, n, H, pat):
     specs, (q, k, v) = _inputs(61, B, n, H)
     scale = 1.0 / np.sqrt(DQK)
