@@ -382,6 +382,26 @@ def extra_rows(args, q, kv, o, flush, peaks):
         "kernel": "FFMA first version (attn_bwd_simt.cu): correctness path, tensor-core version next",
         "algorithmic_flop": bw_flop}
     del of, osp, dh, oh
+    # non-absorbed (MHA-form) SSA prefill: per-head K/V (192 / 128) at the headline's 32K
+    from inputs import TID_V
+    qm, km, vm = (torch.empty((1, N_PREFILL, H, d), dtype=torch.bfloat16, device=dev) for d in (192, 192, 128))
+    for t_, tid in ((qm, TID_Q), (km, TID_K), (vm, TID_V)):
+        fill_(t_, Spec(seed=0, tensor_id=tid, batch=1, n=N_PREFILL, heads=H, d=t_.shape[-1]))
+    om = torch.empty((1, N_PREFILL, H, 128), dtype=torch.bfloat16, device=dev)
+    t_m = _time_events(lambda: loza.ssa_prefill_mha(qm, km, vm, PATTERN, out=om), 5, 2, flush)
+    t_mf = _time_events(lambda: loza.ssa_prefill_mha(qm, km, vm, out=om, sparse=False), 2, 1, flush)
+    mha_fl = ssa_pairs(N_PREFILL, *PATTERN) * H * 2 * (192 + 128)
+    mha_ffl = full_pairs(N_PREFILL) * H * 2 * (192 + 128)
+    m_ms, mf_ms = float(np.mean(t_m)), float(np.mean(t_mf))
+    out["mha_ssa_prefill_32k"] = {
+        "ms": m_ms, "tokens_per_s": N_PREFILL / (m_ms * 1e-3), "tflops": mha_fl / (m_ms * 1e-3) / 1e12,
+        "frac_tensor": mha_fl / (m_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+        "full_ms": mf_ms, "full_tflops": mha_ffl / (mf_ms * 1e-3) / 1e12,
+        "full_frac_tensor": mha_ffl / (mf_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+        "ssa_vs_full": mf_ms / m_ms,
+        "shape": "B1, 32768 tokens, H64, q/k 192, v 128 per head, (1,7,128); K/V up-projection not included",
+        "algorithmic_flop": mha_fl}
+    del qm, km, vm, om
     if not args.no_cpu:
         try:
             ot = oracle_row_timings()
@@ -559,6 +579,16 @@ def oracle_row_timings(seconds_each: float = 1.5):
     pairs_small = sum(min(t + 1, 1024) for t in range(n_b)) * H  # (1,7,128) window covers all of 256 tokens
     out["backward_ssa_8k"] = {"oracle_ms": dt / pairs_small * ssa_pairs(8192, *PATTERN) * H * 1e3,
                               "sample": f"{n_b} tokens x 64 heads, full backward (two passes)"}
+    # MHA-form SSA: one head, 1024 query rows against their (1,7,128) windows, extrapolated to 32K x 64 heads
+    n_m = 1024
+    qh = gen_rows_f32(Spec(seed=0, tensor_id=TID_Q, batch=1, n=n_m, heads=1, d=192), 0, n_m)
+    kh = gen_rows_f32(Spec(seed=0, tensor_id=TID_K, batch=1, n=n_m, heads=1, d=192), 0, n_m)
+    vh = np.ascontiguousarray(kh[:, :128])
+    t0 = time.perf_counter()
+    oracle.attention_rows(qh, np.arange(n_m), kh, vh, 1.0 / np.sqrt(192.0), *PATTERN)
+    dt = time.perf_counter() - t0
+    out["mha_ssa_prefill_32k"] = {"oracle_ms": dt / ssa_pairs(n_m, *PATTERN) * ssa_pairs(N_PREFILL, *PATTERN) * H
+                                  * 1e3, "sample": f"{n_m} tokens x 1 head (d 192 / 128)"}
     return out
 
 
