@@ -103,6 +103,10 @@ constexpr uint32_t kTmemO = 0, kTmemS = 256;  // S buffer b at 256 + 128 b
 constexpr uint32_t kSoftmaxWarps = 8;
 constexpr uint32_t kArrivalsPerPair = 2 * kSoftmaxWarps;
 
+#ifndef MLA_SOFTMAX_V2
+#define MLA_SOFTMAX_V2 1
+#endif
+
 struct PrefillParams {
   CUtensorMap q_map;
   CUtensorMap k_map[3];   // 3-D, box 128 rows x 1 chunk (the RoPE chunk 8)
@@ -128,7 +132,8 @@ struct PrefillParams {
   const float* alpha;
   double* part;            // per-CTA fp64 partial of d_alpha
   int32_t* status;
-  int32_t small;              // all index math fits in uint32 (make_unit fast path)
+  int32_t small;              // all index math fits in 31 bits (make_unit fast path)
+  FastDiv div_upb, div_heads, div_b;  // multiply-shift divisors for the small path
   unsigned long long* trace;  // debug timeline (cluster 0, leader CTA), NULL in production
 };
 
@@ -144,15 +149,17 @@ struct Unit {
 template <typename T>
 __device__ __forceinline__ Unit make_unit_t(const PrefillParams& p, int64_t u64) {
   Unit U;
+  constexpr bool fast = sizeof(T) == 4;
   const T u = (T)u64, upb = (T)p.units_per_batch, heads = (T)p.heads;
-  const T bi = u / upb;
+  const T bi = fast ? (T)p.div_upb.div((uint32_t)u) : u / upb;
   const T row0 = (u - bi * upb) * 128;
   const T rows = (T)p.n_q * heads;
   T rlast = row0 + 127;
   if (rlast > rows - 1) rlast = rows - 1;
   U.bi = (int32_t)bi;
   U.row0 = (int64_t)row0;
-  const T tok_lo = (T)p.q_start + row0 / heads, tok_hi = (T)p.q_start + rlast / heads;
+  const T tok_lo = (T)p.q_start + (fast ? (T)p.div_heads.div((uint32_t)row0) : row0 / heads),
+          tok_hi = (T)p.q_start + (fast ? (T)p.div_heads.div((uint32_t)rlast) : rlast / heads);
   U.tok_lo = (int64_t)tok_lo;
   U.tok_hi = (int64_t)tok_hi;
   const T last_sub = p.causal ? tok_hi / 128 : ((T)p.n_kv - 1) / 128;
@@ -161,7 +168,7 @@ __device__ __forceinline__ Unit make_unit_t(const PrefillParams& p, int64_t u64)
     U.loc_begin = 0;
     U.n128 = (int32_t)(last_sub + 1);
   } else {
-    const int64_t tpb = p.b / 128, QB = (int64_t)(tok_lo / (T)p.b);
+    const int64_t tpb = p.b / 128, QB = (int64_t)(fast ? (T)p.div_b.div((uint32_t)tok_lo) : tok_lo / (T)p.b);
     int64_t sink_end = (QB + 1 < p.s ? QB + 1 : p.s) * tpb;
     if (sink_end > (int64_t)last_sub + 1) sink_end = (int64_t)last_sub + 1;
     int64_t lb = QB - p.l + 1;
@@ -550,11 +557,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     constexpr bool calib = kCalib;
     const float alpha = calib ? *p.alpha : 0.f, om_alpha = 1.f - alpha;
     double gacc = 0.0;  // this thread's part of d_alpha (fused calibration with d_o_hat)
+    bool read_pend = false;  // the last epilogue's second store round may still be reading the P buffer
+    // units are decoded one ahead, inside the previous epilogue while a TMA store reads its staging
+    Unit Un = make_unit(p, unit_index(p, cid < n_iter_total ? cid : 0));
     for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
-      const Unit U = make_unit(p, unit_index(p, it));
+      const Unit U = Un;
       const int64_t row_g = U.row0 + 64 * rank + r;
       const bool row_ok = row_g < rows_b;
-      const int64_t my_tok = p.q_start + (row_ok ? row_g : rows_b - 1) / p.heads;
+      const int64_t row_c = row_ok ? row_g : rows_b - 1;
+      const int64_t my_tok = p.q_start + (p.small ? (int64_t)p.div_heads.div((uint32_t)row_c) : row_c / p.heads);
       float m_used = -INFINITY, lrow = 0.f;
       for (int i = 0; i < U.n_tiles; ++i) {
         const uint32_t gi = g + i, buf = gi & 1;
@@ -587,6 +598,18 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
             if (j >= nvalid) v[j] = __float_as_uint(-INFINITY);
         }
         // row max (raw logits; scale > 0 commutes with max), 4 independent chains
+#if MLA_SOFTMAX_V2
+        float mx[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {  // 4 chains of 3-input max (FMNMX3) over v[4 k + c]
+          mx[c] = fmax3(__uint_as_float(v[c]), __uint_as_float(v[4 + c]), __uint_as_float(v[8 + c]));
+#pragma unroll
+          for (int k = 3; k < 15; k += 2)
+            mx[c] = fmax3(mx[c], __uint_as_float(v[4 * k + c]), __uint_as_float(v[4 * k + 4 + c]));
+          mx[c] = fmaxf(mx[c], __uint_as_float(v[60 + c]));
+        }
+        float tmax = fmaxf(fmax3(mx[0], mx[1], mx[2]), mx[3]) * sl2;
+#else
         float mx0 = __uint_as_float(v[0]), mx1 = __uint_as_float(v[1]), mx2 = __uint_as_float(v[2]),
               mx3 = __uint_as_float(v[3]);
 #pragma unroll
@@ -597,16 +620,42 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
         }
         float tmax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+#endif
         float* rb = red + buf * 256;
         rb[q4 * 64 + r] = tmax;
+        if (read_pend) {  // P is written after this barrier: the previous output store must have read it
+          if (warp == 2 && lane == 0) bulk_wait_group_read0();
+          read_pend = false;
+        }
         named_bar_sync(1, kSmThreads);
         tmax = fmaxf(fmaxf(rb[r], rb[64 + r]), fmaxf(rb[128 + r], rb[192 + r]));
         const bool resc = tmax > m_used + 8.0f;
         const float m_new = resc ? tmax : m_used;
         const float corr = resc ? ex2(m_used - m_new) : 1.0f;
         // P = exp2(s * scale - m): 4 independent partial sums; packed to bf16 pairs
-        float ps0 = 0.f, ps1 = 0.f, ps2 = 0.f, ps3 = 0.f;
         uint32_t pk[32];
+#if MLA_SOFTMAX_V2
+        // scale-subtract and row sums on pairs (FFMA2 / FADD2): half the FP32 instructions of the scalar form
+        float ps0, ps1, ps2 = 0.f, ps3 = 0.f;
+        {
+          const uint64_t sl2v = f2pack(sl2, sl2), nmv = f2pack(-m_new, -m_new);
+          uint64_t acc0 = f2pack(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float y0, y1;
+            f2unpack(ffma2(f2pack(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])), sl2v, nmv), y0, y1);
+            const float e0 = ex2(y0), e1 = ex2(y1);
+            const uint64_t e = f2pack(e0, e1);
+            if (j & 1)
+              acc1 = fadd2(acc1, e);
+            else
+              acc0 = fadd2(acc0, e);
+            pk[j] = pack_bf16x2(e0, e1);
+          }
+          f2unpack(fadd2(acc0, acc1), ps0, ps1);
+        }
+#else
+        float ps0 = 0.f, ps1 = 0.f, ps2 = 0.f, ps3 = 0.f;
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
           const float e0 = ex2(fmaf(__uint_as_float(v[2 * j]), sl2, -m_new));
@@ -620,6 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           pk[j] = pack_bf16x2(e0, e1);
           pk[j + 1] = pack_bf16x2(e2, e3);
         }
+#endif
         // PV(t-1) must be complete before O is rescaled and before P (single buffer) is overwritten
         if (i > 0) {
           const uint32_t gp = gi - 1;
@@ -720,9 +770,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(ofree);
+        if (warp == 2 && lane == 0) TRACE(17, gl);
         const uint32_t stage = sbase + kOffP;
 #pragma unroll
         for (int rd = 0; rd < 2; ++rd) {  // round rd: the warps with ch == rd, dims [256 rd, +256) = 4 boxes
+          if (rd == 1) {  // round 0's store reads the staging: decode the next unit meanwhile, then wait
+            if (it + ncl < n_iter_total) Un = make_unit(p, unit_index(p, it + ncl));
+            if (warp == 2 && lane == 0) bulk_wait_group_read0();
+            named_bar_sync(1, kSmThreads);
+          }
           if (ch == (uint32_t)rd) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -737,14 +793,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
             fence_proxy_async_smem();
           }
           named_bar_sync(1, kSmThreads);
+          if (warp == 2 && lane == 0) TRACE(18 + 2 * rd, gl);
           if (warp == 2 && lane == 0) {
             for (int m = 0; m < 4; ++m)
               tma_store_3d(&p.o_map, stage + m * 8192, 64 * (4 * rd + m), (int32_t)(U.row0 + 64 * rank), U.bi);
             bulk_commit_group();
-            bulk_wait_group_read0();  // staging may be overwritten
           }
-          named_bar_sync(1, kSmThreads);
+          if (warp == 2 && lane == 0) TRACE(19 + 2 * rd, gl);
         }
+        read_pend = true;  // round 1's read is awaited before the next unit's first P write
       } else {
         char* obase = reinterpret_cast<char*>(p.o) + ((int64_t)U.bi * p.o_sb + (row_ok ? row_g : 0) * kDv) * 4;
 #pragma unroll 1
@@ -766,6 +823,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(ofree);
+        if (it + ncl < n_iter_total) Un = make_unit(p, unit_index(p, it + ncl));
       }
       if (p.lse && row_ok && q4 == 0) {
         const int64_t h = row_g % p.heads, tl_ = row_g / p.heads;
@@ -837,6 +895,11 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
   if (p.total_units == 0) return cudaSuccess;
   const int64_t lim = (int64_t)1 << 31;
   p.small = p.total_units * 128 < lim && rows + 128 < lim && a.q_start + a.n_q + 128 < lim && a.n_kv + 128 < lim;
+  if (p.small) {
+    p.div_upb.init((uint32_t)p.units_per_batch);
+    p.div_heads.init((uint32_t)a.heads);
+    p.div_b.init((uint32_t)(a.sparse ? a.b : 128));
+  }
   if (!encode_3d(&p.q_map, a.q, kDqk, rows, a.batch, kDqk, a.q_sb, 64)) return cudaErrorInvalidValue;
   if (a.out_bf16 && !encode_3d(&p.o_map, a.o, kDv, rows, a.batch, kDv, a.o_sb, 64)) return cudaErrorInvalidValue;
   p.nseg = a.kv.nseg;

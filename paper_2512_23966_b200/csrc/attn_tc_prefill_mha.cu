@@ -67,19 +67,6 @@ constexpr uint32_t kSoftmaxWarps = 8;
 constexpr uint32_t kPolyPairs = MHA_POLY_PAIRS;  // exp pairs (of 32 per thread and tile) computed by polynomial
 constexpr uint32_t kArrivalsPerPair = 2 * kSoftmaxWarps;
 
-// n / d for 0 <= n < 2^31, 1 <= d < 2^31 as one wide multiply + shift (Granlund-Montgomery with
-// m = ceil(2^p / d), p = 31 + ceil(log2 d))
-struct FastDiv {
-  uint32_t m, p;
-  __host__ void init(uint32_t d) {
-    uint32_t l = 0;
-    while ((1ull << l) < d) ++l;
-    p = 31 + l;
-    m = (uint32_t)(((1ull << p) + d - 1) / d);
-  }
-  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (uint32_t)(((uint64_t)n * m) >> p); }
-};
-
 struct MhaParams {
   CUtensorMap q_map;  // 5-D, box 128 tokens x 1 chunk
   CUtensorMap k_map;  // 5-D, box 64 keys x 3 chunks

@@ -293,6 +293,18 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// n / d for 0 <= n < 2^31, 1 <= d < 2^31 as one wide multiply + shift (Granlund-Montgomery with
+// m = ceil(2^p / d), p = 31 + ceil(log2 d)); init() on the host
+struct FastDiv {
+  uint32_t m, p;
+  __host__ void init(uint32_t d) {
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    p = 31 + l;
+    m = (uint32_t)(((1ull << p) + d - 1) / d);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (uint32_t)(((uint64_t)n * m) >> p); }
+};
 // ---- paired fp32 (FFMA2 / FADD2) and 3-input max (FMNMX3), sm_100
 __device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
   uint64_t r;
