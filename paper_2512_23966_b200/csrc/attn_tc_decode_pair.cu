@@ -28,8 +28,9 @@ using namespace sm100;
 
 constexpr int kDqk = 576, kDv = 512, kChunks = 9, kH = 64;
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 softmax / merge
-constexpr int kStageBytes = 16384;
-constexpr int kStages = 7;
+constexpr int kStageBytes = 32768;  // ring item: 2 K chunks (128 keys x 128 dims) or 2 V slabs (64 keys x 256 dims)
+constexpr int kStages = 3;
+constexpr int kHalf = 16384;
 constexpr int kQBytes = kChunks * 64 * 128;  // 73728
 constexpr int kPBytes = 2 * 64 * 128;        // 16384 per buffer: P [128 keys][64 heads] bf16
 constexpr int kOffQ = 0;
@@ -57,9 +58,10 @@ constexpr int kSendO = 2 * 128 * 2 * 128;        // [2 groups][128 dims][2 head 
 constexpr int kSendBytes = kSendO + 2 * 64 * 4;  // + m[64], l[64]
 constexpr int kOffSend = kOffQ;                  // own Q region
 constexpr int kOffRecv = kOffRing;               // partner writes into this CTA's ring
-constexpr int kOffOut = kOffRing + ((kSendBytes + 1023) & ~1023);  // bf16 [4 boxes][64 heads][64 dims]
+constexpr int kOffOut = kOffP;                   // bf16 [4 boxes][64 heads][64 dims] in the idle P buffers
 static_assert(kSendBytes <= kQBytes, "send staging fits the Q region");
-static_assert(kOffOut + 4 * 8192 <= kOffRing + kStages * kStageBytes, "recv + out staging fit the ring");
+static_assert(kSendBytes <= kStages * kStageBytes, "receive staging fits the ring");
+static_assert(4 * 8192 <= 2 * kPBytes, "output staging fits the P buffers");
 
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kTmemS = 256;  // S^T buffer b: 128 lanes (keys) x 64 cols (heads) at 256 + 64 b
@@ -219,25 +221,31 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         phase ^= 1;
       }
     };
+    // 32 KB items (half the per-item wait/commit overhead of 16 KB items): K chunks {2j, 2j + 1} (chunk 8
+    // alone), V slabs of keys 64 kp .. 64 kp + 63 (two 32-key boxes) x dim chunks 4 nh .. 4 nh + 3
     auto load_k = [&](int32_t k0) {
-      for (int cc = 0; cc < kChunks; ++cc) {
+      for (int j = 0; j < (kChunks + 1) / 2; ++j) {
         const uint32_t dst = acquire();
+        const int nc = 2 * j + 1 < kChunks ? 2 : 1;
         if (elect_one()) {
-          mbar_arrive_expect_tx(bar(kBarRingFull + stage), kStageBytes);
-          tma_load_3d(dst, &p.k_map, cc * 64, k0, bi, bar(kBarRingFull + stage), pol_kv);
+          mbar_arrive_expect_tx(bar(kBarRingFull + stage), nc * kHalf);
+          for (int sub = 0; sub < nc; ++sub)
+            tma_load_3d(dst + kHalf * sub, &p.k_map, (2 * j + sub) * 64, k0, bi, bar(kBarRingFull + stage), pol_kv);
         }
         __syncwarp();
         next();
       }
     };
     auto load_v = [&](int32_t k0) {
-      for (int kq = 0; kq < 4; ++kq)
+      for (int kp = 0; kp < 2; ++kp)
         for (int nh = 0; nh < 2; ++nh) {
           const uint32_t dst = acquire();
           if (elect_one()) {
             mbar_arrive_expect_tx(bar(kBarRingFull + stage), kStageBytes);
-            // one 4-D box: 32 keys x dim chunks 4 nh .. 4 nh + 3 (smem [chunk][32 keys][64 dims])
-            tma_load_4d(dst, &p.v_map, 0, k0 + 32 * kq, 4 * nh, bi, bar(kBarRingFull + stage), pol_kv);
+            // 4-D boxes: 32 keys x dim chunks 4 nh .. 4 nh + 3 (smem [chunk][32 keys][64 dims]) per half
+            for (int sub = 0; sub < 2; ++sub)
+              tma_load_4d(dst + kHalf * sub, &p.v_map, 0, k0 + 32 * (2 * kp + sub), 4 * nh, bi,
+                          bar(kBarRingFull + stage), pol_kv);
           }
           __syncwarp();
           next();
@@ -271,17 +279,22 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       tc_fence_after();
       const uint32_t d = tmem + kTmemS + 64 * buf;
       long long kw = 0;
-      for (int cc = 0; cc < kChunks; ++cc) {
+      for (int j = 0; j < (kChunks + 1) / 2; ++j) {
+        const int nc = 2 * j + 1 < kChunks ? 2 : 1;
         const long long w0 = clock64();
-        if (gi == 0) mbar_wait(bar(kBarQFull + cc), 0);
+        if (gi == 0)
+          for (int sub = 0; sub < nc; ++sub) mbar_wait(bar(kBarQFull + 2 * j + sub), 0);
         mbar_wait(bar(kBarRingFull + stage), phase);
         kw += clock64() - w0;
         tc_fence_after();
         if (elect_one()) {
+          for (int sub = 0; sub < nc; ++sub) {
+            const int cc = 2 * j + sub;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16_1sm(d, dr_k + (uint64_t)((kStageBytes * stage + 32 * k) >> 4),
-                          dq + (uint64_t)((8192 * cc + 32 * k) >> 4), idesc_s, (cc | k) != 0);
+            for (int k = 0; k < 4; ++k)
+              umma_bf16_1sm(d, dr_k + (uint64_t)((kStageBytes * stage + kHalf * sub + 32 * k) >> 4),
+                            dq + (uint64_t)((8192 * cc + 32 * k) >> 4), idesc_s, (cc | k) != 0);
+          }
           umma_commit_1sm(bar(kBarRingEmpty + stage));
         }
         __syncwarp();
@@ -299,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       DTRACE(4, gi);
       tc_fence_after();
       long long vw = 0;
-      for (int kq = 0; kq < 4; ++kq)
+      for (int kp = 0; kp < 2; ++kp)
         for (int nh = 0; nh < 2; ++nh) {
           const long long w0 = clock64();
           mbar_wait(bar(kBarRingFull + stage), phase);
@@ -307,13 +320,17 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < 2; ++kk)
+            for (int sub = 0; sub < 2; ++sub) {
+              const int kq = 2 * kp + sub;
 #pragma unroll
-              for (int dg = 0; dg < 2; ++dg)
-                umma_bf16_1sm(tmem + 64 * (2 * nh + dg),
-                              dr_v + (uint64_t)((kStageBytes * stage + 8192 * dg + 2048 * kk) >> 4),
-                              dp + (uint64_t)((buf * kPBytes + (32 * kq + 16 * kk) * 128) >> 4), idesc_pv,
-                              !(first && kq == 0 && kk == 0));
+              for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+                for (int dg = 0; dg < 2; ++dg)
+                  umma_bf16_1sm(tmem + 64 * (2 * nh + dg),
+                                dr_v + (uint64_t)((kStageBytes * stage + kHalf * sub + 8192 * dg + 2048 * kk) >> 4),
+                                dp + (uint64_t)((buf * kPBytes + (32 * kq + 16 * kk) * 128) >> 4), idesc_pv,
+                                !(first && kq == 0 && kk == 0));
+            }
             umma_commit_1sm(bar(kBarRingEmpty + stage));
           }
           __syncwarp();

@@ -293,6 +293,11 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// L2 prefetch of a contiguous global range (bulk, asynchronous; bytes % 16 == 0)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(gptr)), "r"(bytes)
+               : "memory");
+}
 // n / d for 0 <= n < 2^31, 1 <= d < 2^31 as one wide multiply + shift (Granlund-Montgomery with
 // m = ceil(2^p / d), p = 31 + ceil(log2 d)); init() on the host
 struct FastDiv {

@@ -17,6 +17,10 @@ for _ in range(3):
 torch.cuda.synchronize()
 L.loza_debug_set_pair_trace(ctypes.c_void_p(tr.data_ptr()))
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+if len(sys.argv) > 1 and sys.argv[1] == "cold":  # flush L2 so the traced step streams from HBM (as in the bench)
+    fl = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    fl.fill_(1)
+    torch.cuda.synchronize()
 s.record(); loza.ssa_decode(q, cache, seq); e.record()
 torch.cuda.synchronize()
 print("event time (us, incl. host launch gap)", s.elapsed_time(e) * 1e3)

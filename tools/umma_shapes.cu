@@ -4,7 +4,7 @@
 #include "sm100.cuh"
 using namespace loza::sm100;
 
-template <int CG, int M, int N>
+template <int CG, int M, int N, bool AMN = false, bool BMN = false>
 __global__ void __launch_bounds__(128, 1) bench(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sb = smem_u32(smem);
@@ -18,7 +18,7 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, unsigned long long* o
   if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tptr;
-  constexpr uint32_t idesc = idesc_bf16_f32(M, N, false, false);
+  constexpr uint32_t idesc = idesc_bf16_f32(M, N, AMN, BMN);
   const bool leader = CG == 1 || cluster_ctarank() == 0;
   if (threadIdx.x < 32 && leader) {
     unsigned long long t0 = clock64();
@@ -46,12 +46,12 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, unsigned long long* o
   if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc<CG>(tmem, 512); }
 }
 
-template <int CG, int M, int N>
+template <int CG, int M, int N, bool AMN = false, bool BMN = false>
 void run(const char* name) {
   unsigned long long* d;
   cudaMalloc(&d, 148 * 8);
   const int smem = 160 * 1024;
-  cudaFuncSetAttribute(bench<CG, M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(bench<CG, M, N, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148); cfg.blockDim = dim3(128); cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
@@ -59,8 +59,8 @@ void run(const char* name) {
   at[0].val.clusterDim.x = CG; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at; cfg.numAttrs = 1;
   const int iters = 8192;
-  cudaLaunchKernelEx(&cfg, bench<CG, M, N>, iters, d);
-  cudaLaunchKernelEx(&cfg, bench<CG, M, N>, iters, d);
+  cudaLaunchKernelEx(&cfg, bench<CG, M, N, AMN, BMN>, iters, d);
+  cudaLaunchKernelEx(&cfg, bench<CG, M, N, AMN, BMN>, iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[148];
   cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
@@ -71,7 +71,18 @@ void run(const char* name) {
   cudaFree(d);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {  // the decode kernel's shapes: S^T (K-major A and B) and O^T += V^T P (MN-major A and B)
+    run<1, 128, 64>("cg1 M128 N64 KK");
+    run<1, 128, 64, true, true>("cg1 M128 N64 MM");
+    run<1, 128, 64, false, true>("cg1 M128 N64 KM");
+    run<1, 128, 64, true, false>("cg1 M128 N64 MK");
+    run<2, 256, 64>("cg2 M256 N64 KK");
+    run<2, 256, 64, true, true>("cg2 M256 N64 MM");
+    run<1, 128, 128, true, true>("cg1 M128 N128 MM");
+    run<2, 128, 256, false, true>("cg2 M128 N256 KM");
+    return 0;
+  }
   run<1, 64, 64>("cg1 M64 N64");
   run<1, 64, 128>("cg1 M64 N128");
   run<1, 64, 256>("cg1 M64 N256");
