@@ -30,8 +30,11 @@ using namespace sm100;
 #define FULL_L(slot) (full_l + 8 * (slot))
 #define QFULL_L(c) (qfull_l + 8 * (c))
 constexpr int kDqk = 192, kDv = 128, kChunks = 3;
-constexpr int kThreads = 352;  // warp 0 Q/K TMA, warp 1 MMA, warps 2-9 softmax/epilogue, warp 10 V TMA
-constexpr int kVWarp = 10;
+// warpgroup 0: warp 0 Q/K TMA, warp 1 MMA, warp 2 V TMA (64 regs); warpgroups 1-2: softmax (warps 4-11,
+// 176 regs); warpgroup 3: epilogue (warps 12-15, 96 regs) -- setmaxnreg rebalances the 128/thread launch
+constexpr int kThreads = 512;
+constexpr int kVWarp = 2;
+constexpr int kSmWarp0 = 4, kEpiWarp0 = 12;
 constexpr int kSlots = 5;
 constexpr int kSlotBytes = 24576;
 constexpr int kKItemBytes = 64 * 128 * kChunks;  // 64 keys x 192 dims
@@ -49,12 +52,16 @@ constexpr int kBarSFull = kBarQEmpty + 2 * kChunks;  // [2]
 constexpr int kBarPFull = kBarSFull + 2;             // [1]
 constexpr int kBarOFull = kBarPFull + 1;             // [2] (tile parity)
 constexpr int kBarOFree = kBarOFull + 2;             // [2] (O buffer = unit parity)
-constexpr int kBarStageFree = kBarOFree + 2;         // [2] (Q buffer = unit parity; local, 2 store issuers)
-constexpr int kNumBars = kBarStageFree + 2;
+constexpr int kBarStageFree = kBarOFree + 2;         // [2] (Q buffer = unit parity; local, 1 store issuer)
+constexpr int kBarOLast = kBarStageFree + 2;         // [2] a unit's last PV landed (O buffer parity)
+constexpr int kBarLFull = kBarOLast + 2;             // [2] softmax -> epilogue: row sums and maxima (local)
+constexpr int kBarLFree = kBarLFull + 2;             // [2] epilogue has read them (local)
+constexpr int kNumBars = kBarLFree + 2;
 constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
 constexpr int kOffPub = kOffTmemPtr + 4;
 constexpr int kOffRed = (kOffPub + 8 + 15) & ~15;
-constexpr int kSmemUsed = kOffRed + 2 * 2 * 128 * 4;
+constexpr int kOffLs = kOffRed + 2 * 2 * 128 * 4;  // float lsum[2 ob][2 ch][128], mrow[2 ob][128]
+constexpr int kSmemUsed = kOffLs + (2 * 2 * 128 + 2 * 128) * 4;
 constexpr int kSmemAlloc = kSmemUsed;
 static_assert(kSmemAlloc <= 232448, "smem");
 
@@ -66,6 +73,7 @@ constexpr uint32_t kSoftmaxWarps = 8;
 #endif
 constexpr uint32_t kPolyPairs = MHA_POLY_PAIRS;  // exp pairs (of 32 per thread and tile) computed by polynomial
 constexpr uint32_t kArrivalsPerPair = 2 * kSoftmaxWarps;
+constexpr uint32_t kEpiArrivalsPerPair = 2 * 4;
 
 struct MhaParams {
   CUtensorMap q_map;  // 5-D, box 128 tokens x 1 chunk
@@ -155,8 +163,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(kBarSFull + i), 1);
       mbar_init(bar(kBarOFull + i), 1);
-      mbar_init(bar(kBarOFree + i), kArrivalsPerPair);
-      mbar_init(bar(kBarStageFree + i), 2);
+      mbar_init(bar(kBarOFree + i), kEpiArrivalsPerPair);
+      mbar_init(bar(kBarStageFree + i), 1);
+      mbar_init(bar(kBarOLast + i), 1);
+      mbar_init(bar(kBarLFull + i), kSoftmaxWarps);
+      mbar_init(bar(kBarLFree + i), 4);
     }
     mbar_init(bar(kBarPFull), kArrivalsPerPair);
     reinterpret_cast<volatile uint32_t*>(smem + kOffPub)[0] = 0;
@@ -202,6 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     __syncwarp();
     mbar_wait(bar(kBarEmpty + rp.slot), rp.phase ^ 1);
   };
+  if (warp < kSmWarp0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
   if (warp == 0) {
     // ===================================================== Q + K items producer (both CTAs)
     const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
@@ -309,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         rp.step();
       };
       // PV of tile gi of unit u (first: the unit's first tile, overwrites O buffer u & 1)
-      auto issue_pv = [&](uint32_t gi, uint32_t u, bool first) {
+      auto issue_pv = [&](uint32_t gi, uint32_t u, bool first, bool last) {
         const uint32_t ob = u & 1;
         MTRACE(3, gi);
         mbar_wait(bar(kBarPFull), gi & 1);
@@ -328,107 +341,116 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           }
           umma_commit_pair_mc(bar(kBarEmpty + slot), 3);
           umma_commit_pair_mc(bar(kBarOFull + (gi & 1)), 3);
+          if (last) umma_commit_pair_mc(bar(kBarOLast + ob), 3);
         }
         __syncwarp();
         rp.step();
       };
       uint32_t pv_u = 0;
-      bool pv_first = false, have_pv = false;
+      bool pv_first = false, pv_last = false, have_pv = false;
       for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
         const Unit U = make_unit(p, unit_index(p, it));
         for (int i = 0; i < U.n_tiles; ++i, ++g) {
           issue_s(g, uc, i == 0, i == U.n_tiles - 1);
-          if (have_pv) issue_pv(g - 1, pv_u, pv_first);
+          if (have_pv) issue_pv(g - 1, pv_u, pv_first, pv_last);
           have_pv = true;
           pv_u = uc;
           pv_first = i == 0;
+          pv_last = i == U.n_tiles - 1;
         }
       }
-      if (have_pv) issue_pv(g - 1, pv_u, pv_first);
+      if (have_pv) issue_pv(g - 1, pv_u, pv_first, pv_last);
     }
-  } else {
-    // ===================================================== softmax + epilogue (warps 2..9, both CTAs)
-    // lane tl = 32 wq + lane holds row tl; warps with ch take keys / O dims [64 ch, 64 ch + 64). The two warps
-    // of a row (wq, ch = 0 / 1) exchange row maxima through smem under named barrier 1 + wq (64 threads).
-    // A unit's epilogue is deferred until after the next unit's first tile (O is double-buffered in TMEM), so
-    // the tensor pipe gets the next P without waiting for the output stores.
-    const uint32_t wq = warp & 3;
-    const uint32_t ch = (warp - 2) >> 2;
-    const uint32_t r = wq * 32 + lane;
+  }
+  } else if (warp >= kEpiWarp0) {
+    // ===================================================== epilogue warpgroup (warps 12..15, both CTAs)
+    // Row r = 32 (warp % 4) + lane, all 128 dims: waits for the unit's row sums (LFull) and last PV (OLast),
+    // reads O from TMEM and releases it, stages bf16 [128 x 64] boxes in the unit's dead Q buffer and
+    // TMA-stores them; off the softmax warps' path entirely.
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
+    const uint32_t wq = warp & 3, r = wq * 32 + lane;
     const uint32_t taddr = tmem + ((wq * 32) << 16);
-    const uint32_t pfull = mapa(bar(kBarPFull), 0), ofree0 = mapa(bar(kBarOFree), 0);
+    const uint32_t ofree0 = mapa(bar(kBarOFree), 0);
+    const float* lsm = reinterpret_cast<const float*>(smem + kOffLs);
     const float ln2 = 0.69314718055994531f;
-    const float sl2 = p.scale_log2;
-    const int causal = p.causal, sparse = p.sparse;
-    const int64_t n_kv = p.n_kv, sink_keys = (int64_t)p.s * p.b;
-    const uint32_t pair_bar = 1 + wq;
-    // pending epilogue (unit pe_u)
-    bool pend = false, stage_pend = false;
-    uint32_t stage_qb = 0;
-    uint32_t pe_u = 0;
-    int32_t pe_b = 0, pe_h = 0;
-    int64_t pe_row0 = 0;
-    float pe_m = 0.f, pe_l = 0.f;
-    auto epilogue = [&](uint32_t g_cur, bool g_cur_is_next) {
-      // g_cur: the last tile whose pair barrier this thread passed; red buffer (g_cur + 1) & 1 is free
-      float* ls = red + ((g_cur + 1) & 1) * 256;
-      ls[ch * 128 + r] = pe_l;
-      named_bar_sync(pair_bar, 64);
-      const float ltot = pe_l + ls[(ch ^ 1) * 128 + r];
-      named_bar_sync(pair_bar, 64);
-      const float inv = 1.0f / ltot;
-      const uint32_t ob = pe_u & 1;
-      uint32_t ov[64];
-      const uint32_t gl = g_cur - (g_cur_is_next ? 1 : 0);  // the unit's last tile
-      mbar_wait(bar(kBarOFull + (gl & 1)), (gl >> 1) & 1);
-      tc_fence_after();
-      tmem_ld32(taddr + kTmemO + 128 * ob + 64 * ch, *reinterpret_cast<uint32_t(*)[32]>(&ov[0]));
-      tmem_ld32(taddr + kTmemO + 128 * ob + 64 * ch + 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[32]));
-      tmem_wait_ld();
-      tc_fence_before();
+    uint32_t uc = 0, g = 0;
+    for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
+      const Unit U = make_unit(p, unit_index(p, it));
+      const uint32_t ob = uc & 1, par = (uc >> 1) & 1;
+      g += U.n_tiles;
+      mbar_wait(bar(kBarLFull + ob), par);
+      const float ltot = lsm[(2 * ob) * 128 + r] + lsm[(2 * ob + 1) * 128 + r];
+      const float mrow = lsm[512 + ob * 128 + r];
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(ofree0 + 8 * ob);
-      const int64_t row_g = pe_row0 + 128 * rank + r;
+      if (lane == 0) mbar_arrive_local(bar(kBarLFree + ob));
+      const float inv = 1.0f / ltot;
+      mbar_wait(bar(kBarOLast + ob), par);
+      tc_fence_after();
+      const int64_t row_g = U.row0 + 128 * rank + r;
       const bool row_ok = row_g < p.n_q;
-      if (p.out_bf16) {
-        // box ch = dims [64 ch, +64) staged in chunk ch of the unit's (dead) Q buffer, swizzled by r & 7
-        const uint32_t stage = sbase + kOffQ + kQBytes * ob + ch * kQChunkBytes;
-        const uint32_t box = stage + r * 128;
+      const uint32_t stage = sbase + kOffQ + kQBytes * ob;  // the unit's Q buffer (its last S has completed)
+      float* dst = reinterpret_cast<float*>(p.o) + (int64_t)U.bi * p.o_sb + row_g * p.o_st + (int64_t)U.h * p.o_sh;
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          st_shared_v4(box + ((q ^ (r & 7)) << 4),
-                       pack_bf16x2(__uint_as_float(ov[8 * q]) * inv, __uint_as_float(ov[8 * q + 1]) * inv),
-                       pack_bf16x2(__uint_as_float(ov[8 * q + 2]) * inv, __uint_as_float(ov[8 * q + 3]) * inv),
-                       pack_bf16x2(__uint_as_float(ov[8 * q + 4]) * inv, __uint_as_float(ov[8 * q + 5]) * inv),
-                       pack_bf16x2(__uint_as_float(ov[8 * q + 6]) * inv, __uint_as_float(ov[8 * q + 7]) * inv));
-        fence_proxy_async_smem();
-        named_bar_sync(5 + ch, 128);
-        if (wq == 0 && lane == 0) {
-          tma_store_5d(&p.o_map, stage, 0, (int32_t)(pe_row0 + 128 * rank), (int)ch, pe_h, pe_b);
-          bulk_commit_group();
-        }
-        // StageFree (the Q buffer may be reloaded for unit pe_u + 2) is signalled after the store has read the
-        // staging, a few tiles later (a wait here would stall the softmax behind the TMA queue)
-        stage_pend = true;
-        stage_qb = ob;
-      } else {
-        if (row_ok) {
-          float* dst = reinterpret_cast<float*>(p.o) + (int64_t)pe_b * p.o_sb + row_g * p.o_st +
-                       (int64_t)pe_h * p.o_sh + 64 * ch;
+      for (int c = 0; c < 4; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(taddr + kTmemO + 128 * ob + 32 * c, ov);
+        tmem_wait_ld();
+        if (p.out_bf16) {
+          const uint32_t box = stage + (c >> 1) * kQChunkBytes + r * 128;
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            st_global_v4(dst + 4 * q, __float_as_uint(__uint_as_float(ov[4 * q]) * inv),
+          for (int q = 0; q < 4; ++q)
+            st_shared_v4(box + ((((c & 1) * 4 + q) ^ (r & 7)) << 4),
+                         pack_bf16x2(__uint_as_float(ov[8 * q]) * inv, __uint_as_float(ov[8 * q + 1]) * inv),
+                         pack_bf16x2(__uint_as_float(ov[8 * q + 2]) * inv, __uint_as_float(ov[8 * q + 3]) * inv),
+                         pack_bf16x2(__uint_as_float(ov[8 * q + 4]) * inv, __uint_as_float(ov[8 * q + 5]) * inv),
+                         pack_bf16x2(__uint_as_float(ov[8 * q + 6]) * inv, __uint_as_float(ov[8 * q + 7]) * inv));
+        } else if (row_ok) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            st_global_v4(dst + 32 * c + 4 * q, __float_as_uint(__uint_as_float(ov[4 * q]) * inv),
                          __float_as_uint(__uint_as_float(ov[4 * q + 1]) * inv),
                          __float_as_uint(__uint_as_float(ov[4 * q + 2]) * inv),
                          __float_as_uint(__uint_as_float(ov[4 * q + 3]) * inv));
         }
-        __syncwarp();
-        if (wq == 0 && lane == 0) mbar_arrive_local(bar(kBarStageFree + ob));
       }
-      if (p.lse && row_ok && ch == 0)
-        p.lse[((int64_t)pe_b * p.heads + pe_h) * p.n_q + row_g] = (pe_m + __log2f(ltot)) * ln2;
-      pend = false;
-    };
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(ofree0 + 8 * ob);
+      if (warp == kEpiWarp0) MTRACE(9, g - 1);
+      if (p.out_bf16) {
+        fence_proxy_async_smem();
+        named_bar_sync(7, 128);
+        if (warp == kEpiWarp0 && lane == 0) {
+          for (int m = 0; m < 2; ++m)
+            tma_store_5d(&p.o_map, stage + m * kQChunkBytes, 0, (int32_t)(U.row0 + 128 * rank), m, U.h, U.bi);
+          bulk_commit_group();
+          bulk_wait_group_read0();  // then the Q buffer may be reloaded (unit uc + 2)
+          mbar_arrive_local(bar(kBarStageFree + ob));
+        }
+      } else {
+        named_bar_sync(7, 128);
+        if (warp == kEpiWarp0 && lane == 0) mbar_arrive_local(bar(kBarStageFree + ob));
+      }
+      if (p.lse && row_ok) p.lse[((int64_t)U.bi * p.heads + U.h) * p.n_q + row_g] = (mrow + __log2f(ltot)) * ln2;
+    }
+    if (warp == kEpiWarp0 && lane == 0) bulk_wait_group0();
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 176;");
+    // ===================================================== softmax (warps 4..11, both CTAs)
+    // lane tl = 32 wq + lane holds row tl; warps with ch take keys / O dims [64 ch, 64 ch + 64). The two warps
+    // of a row (wq, ch = 0 / 1) exchange row maxima through smem under named barrier 1 + wq (64 threads).
+    // At a unit's end the row's partial sums and max go to the epilogue warpgroup (O is double-buffered in
+    // TMEM, so the next unit's tiles proceed while it drains).
+    const uint32_t wq = warp & 3;
+    const uint32_t ch = (warp - kSmWarp0) >> 2;
+    const uint32_t r = wq * 32 + lane;
+    const uint32_t taddr = tmem + ((wq * 32) << 16);
+    const uint32_t pfull = mapa(bar(kBarPFull), 0);
+    const float sl2 = p.scale_log2;
+    const int causal = p.causal, sparse = p.sparse;
+    const int64_t n_kv = p.n_kv, sink_keys = (int64_t)p.s * p.b;
+    const uint32_t pair_bar = 1 + wq;
+    float* lsm = reinterpret_cast<float*>(smem + kOffLs);
     uint32_t g = 0, uc = 0;
     for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
       const Unit U = make_unit(p, unit_index(p, it));
@@ -449,18 +471,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         if (causal && my_tok + 1 - c0 < lim) lim = my_tok + 1 - c0;
         if (c0 >= sink_keys && c0 < win_lo) lim = 0;
         const int32_t nvalid = lim < 0 ? 0 : (lim > 64 ? 64 : (int32_t)lim);
-        // the previous epilogue's store has long read its staging by the unit's 4th-last tile; flushing there
-        // (not at the next tile) keeps the wait off the softmax path, and is still ahead of the Q(u + 2) load
-        if (stage_pend && (i == 0 || i + 3 >= U.n_tiles)) {
-          if (wq == 0 && lane == 0) {
-            bulk_wait_group_read0();
-            mbar_arrive_local(bar(kBarStageFree + stage_qb));
-          }
-          stage_pend = false;
-        }
         mbar_wait(bar(kBarSFull + buf), (g >> 1) & 1);
         tc_fence_after();
-        if (warp == 2) MTRACE(6, g);
+        if (warp == kSmWarp0) MTRACE(6, g);
         const uint32_t sa = taddr + kTmemS + 128 * buf + 64 * ch;
         uint32_t v[64];
         tmem_ld32(sa, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
@@ -518,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           const uint32_t gp = g - 1;
           mbar_wait(bar(kBarOFull + (gp & 1)), (gp >> 1) & 1);
           tc_fence_after();
-          if (warp == 2) MTRACE(7, g);
+          if (warp == kSmWarp0) MTRACE(7, g);
           {
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
@@ -541,22 +554,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(pfull);
-        if (warp == 2) MTRACE(8, g);
-        if (pend) {
-          epilogue(g, true);
-          if (warp == 2) MTRACE(9, g);
-        }  // the previous unit's O is complete (PV(g - 1) waited above)
+        if (warp == kSmWarp0) MTRACE(8, g);
       }
-      pend = true;
-      pe_u = uc;
-      pe_b = U.bi;
-      pe_h = U.h;
-      pe_row0 = U.row0;
-      pe_m = m_used;
-      pe_l = lrow;
+      // the unit's row sums / max to the epilogue warpgroup (after it has read unit uc - 2's)
+      mbar_wait(bar(kBarLFree + ob), ((uc >> 1) & 1) ^ 1);
+      lsm[(2 * ob + ch) * 128 + r] = lrow;
+      if (ch == 0) lsm[512 + ob * 128 + r] = m_used;
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(bar(kBarLFull + ob));
     }
-    if (pend) epilogue(g - 1, false);
-    if (wq == 0 && lane == 0) bulk_wait_group0();
   }
   __syncwarp();
   tc_fence_before();
