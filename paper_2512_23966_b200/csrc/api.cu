@@ -298,7 +298,7 @@ loza_status_t ssa_decode_ring(const loza_attn_args_t* args, const int32_t* seq_l
   if (path != Path::kTc || !decode_pair_eligible(p, device_sm_count()))
     return fail(LOZA_ERR_UNSUPPORTED, "ring decode: bf16, H == 64, b %% 128 == 0, 2*batch <= SMs");
   p.ring = 1;
-  return cuda_status(launch_decode_pair(p, (cudaStream_t)stream), "decode_pair (ring) launch");
+  return cuda_status(launch_decode_pair_any(p, (cudaStream_t)stream), "decode_pair (ring) launch");
 }
 
 loza_status_t ssa_select_blocks(int64_t n_q, int64_t q_start, loza_pattern_t pat, int32_t causal, int32_t* idx_dev,

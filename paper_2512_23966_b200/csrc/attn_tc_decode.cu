@@ -609,7 +609,7 @@ size_t decode_tc_ws_bytes(const AttnProblem& a) {
 unsigned long long* g_decode_trace = nullptr;
 
 cudaError_t launch_decode_tc(const AttnProblem& a, void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (decode_pair_eligible(a, device_sm_count())) return launch_decode_pair(a, st);
+  if (decode_pair_eligible(a, device_sm_count())) return launch_decode_pair_any(a, st);
   if (a.ring) return cudaErrorNotSupported;  // the ring cache is read by the pair kernel only
   if (a.heads != kH) return cudaErrorNotSupported;
   if (a.batch > kMaxBatch) return cudaErrorNotSupported;

@@ -16,6 +16,7 @@
 //    tools/dsmem_bw.cu, vs ~15 for st.shared::cluster and ~11 through L2); all 8 softmax warps combine,
 //    stage bf16 [64 heads x 64 dims] swizzled boxes and TMA-store them.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "internal.h"
@@ -617,6 +618,16 @@ cudaError_t launch_decode_pair(const AttnProblem& a, cudaStream_t st) {
   if (le != cudaSuccess) return le;
   count_launch();
   return cudaGetLastError();
+}
+
+// pair mode: the key-split pair kernel above; LOZA_DECODE_KERNEL=coop selects the pair-cooperative kernel
+// (attn_tc_decode_coop.cu: correct, -0.7% cold / -4.5% L2-warm per step, not adopted)
+cudaError_t launch_decode_pair_any(const AttnProblem& a, cudaStream_t st) {
+  static const int use_coop = [] {
+    const char* e = getenv("LOZA_DECODE_KERNEL");
+    return e && strcmp(e, "coop") == 0 ? 1 : 0;
+  }();
+  return use_coop ? launch_decode_coop(a, st) : launch_decode_pair(a, st);
 }
 
 // pair mode: SSA, 64 heads, whole-tile blocks, and 2 CTAs per sequence fit in one wave

@@ -64,6 +64,9 @@ cudaError_t launch_dalpha_reduce(const double* part, int n, const float* alpha, 
 // tcgen05 paths (bf16, d_qk 576, d_v 512)
 cudaError_t launch_prefill_tc(const AttnProblem& p, cudaStream_t st);
 // non-absorbed (MHA) form, d_qk 192 / d_v 128, per-head K/V (k_sh, v_sh: head strides in elements)
+// pair-cooperative SSA decode (attn_tc_decode_coop.cu): same eligibility as the pair kernel
+cudaError_t launch_decode_coop(const AttnProblem& a, cudaStream_t st);
+cudaError_t launch_decode_pair_any(const AttnProblem& a, cudaStream_t st);
 cudaError_t launch_prefill_mha(const AttnProblem& a, int64_t k_sh, int64_t v_sh, cudaStream_t st);
 cudaError_t launch_decode_tc(const AttnProblem& p, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t decode_tc_ws_bytes(const AttnProblem& p);
