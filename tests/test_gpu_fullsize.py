@@ -104,3 +104,26 @@ def test_seqpar_8_virtual_ranks_bitwise():
                                           prev_k=shards[r - 1] if r > 0 else None)
         torch.cuda.synchronize()
         assert torch.equal(o, ref[:, r * n_local:(r + 1) * n_local]), r
+
+
+def test_mha_prefill_32k_sampled():
+    """MHA-form SSA prefill at the bench shape: B1, 32768 tokens, H64, q/k 192, v 128,
+    (1,7,128); sampled (token, head) rows against the oracle over the token's window."""
+    from inputs import TID_V
+    n, Hm = 32768, 64
+    specs = [Spec(seed=55, tensor_id=t, batch=1, n=n, heads=Hm, d=d) for t, d in ((TID_Q, 192), (TID_K, 192), (TID_V, 128))]
+    q, k, v = (empty_filled(s, four_d=True) for s in specs)
+    o = loza.ssa_prefill_mha(q, k, v, PAT)
+    torch.cuda.synchronize()
+    s, l, b = PAT
+    scale = 1.0 / np.sqrt(192.0)
+    for t, h in [(0, 0), (127, 5), (1023, 63), (1024, 17), (20000, 31), (32767, 2)]:
+        keys = oracle.allowed_keys(t, n, s, l, b)
+        kb = sorted({int(j) // b for j in keys})
+        kk = np.concatenate([gen_rows_f32(specs[1], blk * b * Hm, b * Hm).reshape(b, Hm, 192)[:, h] for blk in kb])
+        vv = np.concatenate([gen_rows_f32(specs[2], blk * b * Hm, b * Hm).reshape(b, Hm, 128)[:, h] for blk in kb])
+        pos = np.concatenate([np.arange(blk * b, blk * b + b) for blk in kb])
+        sel = np.isin(pos, keys)
+        qr = gen_rows_f32(specs[0], t * Hm + h, 1)
+        ref, _ = oracle.attend(qr, kk[sel], vv[sel], scale)
+        assert np.abs(o[0, t, h].double().cpu().numpy() - ref[0]).max() <= 2e-2, (t, h)
