@@ -17,6 +17,7 @@
 //    MMA order K(0), K(1), V(0), K(2), V(1), ...; pair TMA with completion on the leader's barriers);
 //    warp 1 of the leader issues every UMMA; warps 2-9 of both CTAs run the softmax.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "internal.h"
@@ -36,7 +37,9 @@ constexpr int kQBytes = kChunks * kQChunk;       // 36864
 constexpr int kPBytes = 256 * 64;                // [256 keys][32 heads] bf16 per buffer
 constexpr int kOffQ = 0;
 constexpr int kOffP = kOffQ + kQBytes;           // 2 buffers
-constexpr int kOffRing = kOffP + 2 * kPBytes;    // 69632
+constexpr int kOffPst = kOffP + 2 * kPBytes;     // staging of the partner's P rows [2 buf][128 keys][32 heads]
+constexpr int kPstBytes = 128 * 64;
+constexpr int kOffRing = kOffPst + 2 * kPstBytes;
 constexpr int kOffBar = kOffRing + kStages * kStageBytes;
 constexpr int kBarFull = 0;
 constexpr int kBarEmpty = kBarFull + kStages;
@@ -45,13 +48,15 @@ constexpr int kBarSFull = kBarQFull + kChunks;    // [2]
 constexpr int kBarSFree = kBarSFull + 2;          // [2]
 constexpr int kBarPFull = kBarSFree + 2;          // [2]
 constexpr int kBarOFull = kBarPFull + 2;          // [2]
-constexpr int kBarMax = kBarOFull + 2;            // [2] partner's tile maxima landed (local)
-constexpr int kBarL = kBarMax + 2;                // partner's sums landed (local)
+constexpr int kBarMax = kBarOFull + 2;            // [2] partner's tile maxima landed (bulk copy, local)
+constexpr int kBarPRecv = kBarMax + 2;            // [2] partner's P rows landed in this CTA's P half (local)
+constexpr int kBarL = kBarPRecv + 2;              // partner's sums landed (local)
 constexpr int kNumBars = kBarL + 1;
 constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
 constexpr int kOffRed = (kOffTmemPtr + 4 + 15) & ~15;  // float [2 buf][4 key quarters][64 heads]
 constexpr int kOffX = kOffRed + 2 * 4 * 64 * 4;       // float partner maxima [2 buf][64], partner sums [64]
-constexpr int kOffInv = kOffX + 3 * 64 * 4;           // float 1/l [64]
+constexpr int kOffXl = kOffX + 3 * 64 * 4;            // float own maxima [2 buf][64], own sums [64] (copy sources)
+constexpr int kOffInv = kOffXl + 3 * 64 * 4;          // float 1/l [64]
 constexpr int kSmemUsed = kOffInv + 64 * 4;
 constexpr int kSmemAlloc = kSmemUsed;
 static_assert(kSmemAlloc <= 232448, "smem");
@@ -63,6 +68,7 @@ constexpr uint32_t kTmemO = 0, kTmemS = 128;  // O^T group g at 64 g (lanes = di
 constexpr uint32_t kSoftmaxWarps = 8;
 constexpr uint32_t kSmThreads = 32 * kSoftmaxWarps;
 constexpr uint32_t kArrivalsPerPair = 2 * kSoftmaxWarps;
+constexpr uint32_t kPFullArrivals = kArrivalsPerPair;
 
 struct CoopParams {
   CUtensorMap q_map, k_map, v_map, o_map;
@@ -76,12 +82,13 @@ struct CoopParams {
   int64_t o_sb, o_sh;
   int32_t out_bf16;
   float* lse;
-  unsigned long long* trace;  // debug timeline of cluster 0 (NULL in production): [slot][rank][16]
+  unsigned long long* trace;  // debug timeline of cluster trace_cluster (NULL in production): [slot][rank][16]
+  int32_t trace_cluster;
 };
 
 #define CTRACE(slot, idx)                                                                         \
   do {                                                                                            \
-    if (p.trace && blockIdx.x < 2 && (idx) < 16 && (threadIdx.x & 31) == 0)                      \
+    if (p.trace && (int)(blockIdx.x >> 1) == p.trace_cluster && (idx) < 16 && (threadIdx.x & 31) == 0) \
       p.trace[((slot) * 2 + cluster_ctarank()) * 16 + (idx)] = clock64();                       \
   } while (0)
 
@@ -155,11 +162,36 @@ __device__ __forceinline__ void mbar_wait_acquire_cluster(uint32_t bar, uint32_t
         : "memory");
   } while (!ok);
 }
+__device__ __forceinline__ void bulk_copy_to_cluster(uint32_t dst_cluster, uint32_t src, uint32_t bytes,
+                                                     uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_cluster),
+      "r"(src), "r"(bytes), "r"(bar_cluster)
+      : "memory");
+}
+// Spin (mbarrier.test_wait) on a barrier whose phase is completed by the PARTNER's bulk DSMEM copy: a
+// try_wait that suspends is not reliably woken by that remote complete_tx and sleeps to its time limit
+// (measured: ~20 us on a random subset of clusters).
+__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
+  while (!mbar_test(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_cluster() {
   asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
 }
 
 #define FULL_L(slot) (full_l + 8 * (slot))
+#define GSTAMP(k)                                                       \
+  do {                                                                  \
+    if (p.trace && threadIdx.x == 64) {                                 \
+      unsigned long long g_;                                            \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g_));             \
+      p.trace[11 * 2 * 16 + 8 * blockIdx.x + (k)] = g_;                 \
+    }                                                                   \
+  } while (0)
 
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     decode_coop_kernel(const __grid_constant__ CoopParams p) {
@@ -176,6 +208,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   const uint32_t rank = cluster_ctarank(), partner = rank ^ 1;
   const int bi = (int)(blockIdx.x >> 1);
 
+  if (p.trace && threadIdx.x == 0) {  // per-CTA wall-clock span (globaltimer ns) after the timeline slots
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    p.trace[11 * 2 * 16 + 8 * blockIdx.x] = g;
+  }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -186,12 +223,19 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(kBarSFull + i), 1);
       mbar_init(bar(kBarSFree + i), kArrivalsPerPair);
-      mbar_init(bar(kBarPFull + i), kArrivalsPerPair);
+      mbar_init(bar(kBarPFull + i), kPFullArrivals);
       mbar_init(bar(kBarOFull + i), 1);
-      mbar_init(bar(kBarMax + i), 2);  // the partner's two writer warps
+      mbar_init(bar(kBarMax + i), 1);    // armed each tile (expect_tx 256 B), completed by the partner's copies
+      mbar_init(bar(kBarPRecv + i), 1);  // armed each tile (expect_tx 8 KB)
     }
-    mbar_init(bar(kBarL), 2);
+    mbar_init(bar(kBarL), 2);  // the partner's two writer warps
     fence_mbar_init();
+    // every barrier a partner's bulk copy completes is armed BEFORE that copy can arrive (here for the first
+    // phases, then one phase ahead by the thread that consumed the previous one): a complete_tx that reaches
+    // an unarmed barrier was measured to stall the copy by ~20 us
+    for (int i = 0; i < 2; ++i) {
+      mbar_arrive_expect_tx(bar(kBarMax + i), 64 * 4);
+    }
     prefetch_tmap(&p.q_map);
     prefetch_tmap(&p.k_map);
     prefetch_tmap(&p.v_map);
@@ -202,6 +246,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr_smem;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // inputs of the previous kernel are visible from here
+  if (p.trace && threadIdx.x == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    p.trace[11 * 2 * 16 + 8 * blockIdx.x + 1] = g;
+  }
 
   const SeqTiles st = seq_tiles(p, bi);
   const int npt = (st.n_tiles + 1) / 2;  // pair tiles (>= 1)
@@ -263,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       load_v(i - 1);
     }
     load_v(npt - 1);
+    cluster_sync();  // matches the softmax warps' sum exchange
   } else if (warp == 1) {
     // ----------------------------------------------------- UMMA issuer (leader CTA)
     if (rank == 0) {
@@ -311,9 +361,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       auto issue_pv = [&](uint32_t gi, bool first) {
         const uint32_t buf = gi & 1;
         CTRACE(3, gi);
-        mbar_wait(bar(kBarPFull + buf), (gi >> 1) & 1);
-        CTRACE(4, gi);
-        fence_cluster();  // the partner's DSMEM writes of this P half are visible before the MMA reads it
+        mbar_wait_acquire_cluster(bar(kBarPFull + buf), (gi >> 1) & 1);
+
+        CTRACE(4, gi);  // the partner's DSMEM writes of this P half are visible before the MMA reads it
         tc_fence_after();
         for (int q = 0; q < 4; ++q) {
           mbar_wait(bar(kBarFull + slot), phase);
@@ -346,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       }
       issue_pv((uint32_t)(npt - 1), npt == 1);
     }
+    cluster_sync();  // matches the softmax warps' sum exchange
   } else {
     // ----------------------------------------------------- softmax (warps 2..9 of both CTAs)
     // TMEM lane quarter wq = warp % 4: S^T lanes = this CTA's keys 32 wq .. 32 wq + 31 of its sub-block; column
@@ -358,8 +409,6 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     const uint32_t prow = 128 * rank + kl;        // row in the 256-key pair tile
     const float sl2 = p.scale_log2;
     const uint32_t sfree0 = mapa(bar(kBarSFree), 0), pfull0 = mapa(bar(kBarPFull), 0);
-    // P half of CTA ch: local, or the partner's through DSMEM
-    const uint32_t pbase = ch == rank ? sbase + kOffP : mapa(sbase + kOffP, partner);
     float m_used[32], lpart[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
@@ -392,13 +441,18 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       named_bar_sync(1, kSmThreads);
       const float cmax = fmaxf(fmaxf(rb[32 * ch + lane], rb[64 + 32 * ch + lane]),
                                fmaxf(rb[128 + 32 * ch + lane], rb[192 + 32 * ch + lane]));  // this CTA's keys
-      if (wq == 0) {  // send this CTA's maxima for heads 32 ch .. to the partner
-        st_cluster_f32(mapa(sbase + kOffX + (buf * 64 + 32 * ch + lane) * 4, partner), cmax);
+      if (wq == 0) {  // send this CTA's maxima for heads 32 ch .. to the partner (one 128-B bulk DSMEM copy)
+        const uint32_t src = sbase + kOffXl + (buf * 64 + 32 * ch) * 4;
+        st_shared_f32(src + lane * 4, cmax);
+        fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive_release_cluster(mapa(bar(kBarMax + buf), partner));
+        if (lane == 0)
+          bulk_copy_to_cluster(mapa(sbase + kOffX + (buf * 64 + 32 * ch) * 4, partner), src, 128,
+                               mapa(bar(kBarMax + buf), partner));
       }
       if (warp == 2) CTRACE(7, gi);
-      mbar_wait_acquire_cluster(bar(kBarMax + buf), (gi >> 1) & 1);
+      mbar_wait_spin(bar(kBarMax + buf), (gi >> 1) & 1);
+      if (warp == 2 && lane == 0 && i + 2 < npt) mbar_arrive_expect_tx(bar(kBarMax + buf), 64 * 4);  // tile i + 2
       if (warp == 2) CTRACE(8, gi);
       const float hmax = fmaxf(cmax, xch[buf * 64 + 32 * ch + lane]) * sl2;  // shared by both CTAs
       uint32_t pk[16];
@@ -421,15 +475,17 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         lpart[j + 1] = fmaf(lpart[j + 1], corr[j + 1], e1);
         pk[j >> 1] = pack_bf16x2(e0, e1);
       }
-      // P row prow of CTA ch's half: 64 B = 4 x 16-B units, SWIZZLE_64B (unit ^ (row >> 1) & 3)
-      const uint32_t pr = pbase + buf * kPBytes + prow * 64;
+      // P row of CTA ch's half: 64 B = 4 x 16-B units, SWIZZLE_64B (unit ^ (row >> 1) & 3; rows 128 r + kl
+      // and kl share the pattern). Own heads: straight into this CTA's P half; the partner's heads: into the
+      // staging block that one bulk DSMEM copy moves to rows 128 rank .. of the partner's half.
+      const uint32_t pr = (ch == rank ? sbase + kOffP : mapa(sbase + kOffP, partner)) + buf * kPBytes + prow * 64;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint32_t a = pr + ((u ^ ((prow >> 1) & 3)) << 4);
+        const uint32_t ad = pr + ((u ^ ((kl >> 1) & 3)) << 4);
         if (ch == rank)
-          st_shared_v4(a, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          st_shared_v4(ad, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         else
-          st_cluster_v4(a, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          st_cluster_v4(ad, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       }
       if (i > 0) {
         const uint32_t gp = gi - 1;
@@ -453,13 +509,22 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(pfull0 + 8 * buf);
-      } else {  // P rows written into the partner's shared memory, read by the partner's tensor core
+      } else {
         fence_proxy_async_cluster();
-        fence_cluster();
         __syncwarp();
         if (lane == 0) mbar_arrive_release_cluster(pfull0 + 8 * buf);
       }
       if (warp == 2) CTRACE(9, gi);
+    }
+    if (p.trace && threadIdx.x == 64) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+      p.trace[11 * 2 * 16 + 8 * blockIdx.x + 2] = g;
+    }
+    if (p.trace && lane == 0) {  // every softmax warp: left the tile loop
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+      p.trace[11 * 2 * 16 + 8 * 2 * p.batch + 8 * blockIdx.x + (warp - 2)] = g;
     }
     // ---------------- l[h] = this CTA's keys' sum + the partner's; O^T final once the last PV landed
     const uint32_t gl = (uint32_t)(npt - 1);
@@ -475,13 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     ls[wq * 64 + 32 * ch + lane] = lmine;
     named_bar_sync(1, kSmThreads);
     const float lc = (ls[32 * ch + lane] + ls[64 + 32 * ch + lane]) + (ls[128 + 32 * ch + lane] + ls[192 + 32 * ch + lane]);
-    if (wq == 0) {
-      st_cluster_f32(mapa(sbase + kOffX + (128 + 32 * ch + lane) * 4, partner), lc);
-      __syncwarp();
-      if (lane == 0) mbar_arrive_release_cluster(mapa(bar(kBarL), partner));
-    }
+    if (wq == 0) st_cluster_f32(mapa(sbase + kOffX + (128 + 32 * ch + lane) * 4, partner), lc);
     if (warp == 2) CTRACE(10, 0);
-    mbar_wait_acquire_cluster(bar(kBarL), 0);
+    cluster_sync();  // (all warps of both CTAs) the partner's sums landed
+    GSTAMP(4);
     if (warp == 2) CTRACE(10, 1);
     if (wq == 0) {
       const float lt = lc + xch[128 + 32 * ch + lane];
@@ -491,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                                                              __logf(lt);
     }
     mbar_wait(bar(kBarOFull + (gl & 1)), (gl >> 1) & 1);
+    GSTAMP(5);
     tc_fence_after();
     named_bar_sync(1, kSmThreads);  // invl written; every P buffer read (the last PV landed): staging is free
     // O^T (lanes = dims 128 g + 32 wq + lane of this CTA's 256, cols = heads) / l -> bf16 [head][dims] boxes
@@ -522,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       }
     }
     if (warp == 2) CTRACE(10, 2);
+    GSTAMP(6);
     if (p.out_bf16) {
       fence_proxy_async_smem();
       named_bar_sync(1, kSmThreads);
@@ -535,9 +599,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   }
   __syncwarp();
   if (warp == 2) CTRACE(10, 4);
+  GSTAMP(7);
   tc_fence_before();
   cluster_sync();  // every DSMEM write landed before either CTA's shared memory goes away
   if (warp == 2) CTRACE(10, 5);
+  if (p.trace && threadIdx.x == 64) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    p.trace[11 * 2 * 16 + 8 * blockIdx.x + 3] = g;
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<2>(tmem, kTmemCols);
@@ -568,6 +638,10 @@ cudaError_t launch_decode_coop(const AttnProblem& a, cudaStream_t st) {
   p.out_bf16 = a.out_bf16;
   p.lse = a.lse;
   p.trace = g_pair_trace;
+  {
+    const char* e = getenv("LOZA_TRACE_CLUSTER");
+    p.trace_cluster = e ? atoi(e) : 0;
+  }
   const KvSeg& s = a.kv.seg[0];
   if (!encode_3d(&p.q_map, a.q, kDqk, kH, a.batch, a.q_sh, a.q_sb, 32)) return cudaErrorInvalidValue;
   if (!encode_3d(&p.k_map, s.k, kDqk, (uint64_t)a.n_kv, a.batch, s.k_st, s.k_sb, 128)) return cudaErrorInvalidValue;
