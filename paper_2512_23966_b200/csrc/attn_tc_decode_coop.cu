@@ -29,7 +29,8 @@ namespace {
 using namespace sm100;
 
 constexpr int kDqk = 576, kDv = 512, kChunks = 9, kH = 64;
-constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA (leader), warps 2-9 softmax / epilogue
+constexpr int kThreads = 352;  // warp 0 TMA, warp 1 MMA (leader), warps 2-9 softmax / epilogue, warp 10 P transfer
+constexpr int kXferWarp = 10;
 constexpr int kStageBytes = 32768, kHalf = 16384;
 constexpr int kStages = 4;
 constexpr int kQChunk = 32 * 128;                // 32 heads x 64 dims
@@ -49,8 +50,8 @@ constexpr int kBarSFree = kBarSFull + 2;          // [2]
 constexpr int kBarPFull = kBarSFree + 2;          // [2]
 constexpr int kBarOFull = kBarPFull + 2;          // [2]
 constexpr int kBarMax = kBarOFull + 2;            // [2] partner's tile maxima landed (bulk copy, local)
-constexpr int kBarPRecv = kBarMax + 2;            // [2] partner's P rows landed in this CTA's P half (local)
-constexpr int kBarL = kBarPRecv + 2;              // partner's sums landed (local)
+constexpr int kBarPStaged = kBarMax + 2;          // [2] the partner's-heads P rows are staged (4 warps, local)
+constexpr int kBarL = kBarPStaged + 2;              // partner's sums landed (local)
 constexpr int kNumBars = kBarL + 1;
 constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
 constexpr int kOffRed = (kOffTmemPtr + 4 + 15) & ~15;  // float [2 buf][4 key quarters][64 heads]
@@ -68,7 +69,7 @@ constexpr uint32_t kTmemO = 0, kTmemS = 128;  // O^T group g at 64 g (lanes = di
 constexpr uint32_t kSoftmaxWarps = 8;
 constexpr uint32_t kSmThreads = 32 * kSoftmaxWarps;
 constexpr uint32_t kArrivalsPerPair = 2 * kSoftmaxWarps;
-constexpr uint32_t kPFullArrivals = kArrivalsPerPair;
+constexpr uint32_t kPFullArrivals = kArrivalsPerPair + 2;  // + the transfer warp of each CTA
 
 struct CoopParams {
   CUtensorMap q_map, k_map, v_map, o_map;
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       mbar_init(bar(kBarPFull + i), kPFullArrivals);
       mbar_init(bar(kBarOFull + i), 1);
       mbar_init(bar(kBarMax + i), 1);    // armed each tile (expect_tx 256 B), completed by the partner's copies
-      mbar_init(bar(kBarPRecv + i), 1);  // armed each tile (expect_tx 8 KB)
+      mbar_init(bar(kBarPStaged + i), 4);
     }
     mbar_init(bar(kBarL), 2);  // the partner's two writer warps
     fence_mbar_init();
@@ -397,6 +398,27 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       issue_pv((uint32_t)(npt - 1), npt == 1);
     }
     cluster_sync();  // matches the softmax warps' sum exchange
+  } else if (warp == kXferWarp) {
+    // ----------------------------------------------------- P transfer (each CTA): the staged rows of the
+    // partner's heads (8 KB) into rows 128 rank .. of the partner's P half, off the softmax warps' path
+    const uint32_t pfull0 = mapa(bar(kBarPFull), 0);
+    for (int i = 0; i < npt; ++i) {
+      const uint32_t buf = (uint32_t)i & 1;
+      mbar_wait(bar(kBarPStaged + buf), ((uint32_t)i >> 1) & 1);
+      const uint32_t src = sbase + kOffPst + buf * kPstBytes;
+      const uint32_t dst = mapa(sbase + kOffP + buf * kPBytes + 128 * rank * 64, partner);
+#pragma unroll
+      for (int q = 0; q < kPstBytes / 512; ++q) {
+        const uint32_t off = (q * 32 + lane) * 16;
+        uint32_t a, b, c, d;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(src + off));
+        st_cluster_v4(dst + off, a, b, c, d);
+      }
+      fence_proxy_async_cluster();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_release_cluster(pfull0 + 8 * buf);
+    }
+    cluster_sync();  // matches the softmax warps' sum exchange
   } else {
     // ----------------------------------------------------- softmax (warps 2..9 of both CTAs)
     // TMEM lane quarter wq = warp % 4: S^T lanes = this CTA's keys 32 wq .. 32 wq + 31 of its sub-block; column
@@ -478,20 +500,21 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       // P row of CTA ch's half: 64 B = 4 x 16-B units, SWIZZLE_64B (unit ^ (row >> 1) & 3; rows 128 r + kl
       // and kl share the pattern). Own heads: straight into this CTA's P half; the partner's heads: into the
       // staging block that one bulk DSMEM copy moves to rows 128 rank .. of the partner's half.
-      const uint32_t pr = (ch == rank ? sbase + kOffP : mapa(sbase + kOffP, partner)) + buf * kPBytes + prow * 64;
+      const uint32_t pr = ch == rank ? sbase + kOffP + buf * kPBytes + prow * 64 : sbase + kOffPst + buf * kPstBytes + kl * 64;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t ad = pr + ((u ^ ((kl >> 1) & 3)) << 4);
-        if (ch == rank)
-          st_shared_v4(ad, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-        else
-          st_cluster_v4(ad, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      for (int u = 0; u < 4; ++u)
+        st_shared_v4(pr + ((u ^ ((kl >> 1) & 3)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      if (ch != rank) {  // staged for the transfer warp
+        __syncwarp();
+        if (lane == 0) mbar_arrive_local(bar(kBarPStaged + buf));
       }
-      if (i > 0) {
+      // O^T rescale once PV(i - 1) has landed -- only when a head's max moved (the P buffer written above is
+      // free without a wait: S(i) completing implies PV(i - 2) completed, the tensor pipe being in order)
+      if (i > 0 && __any_sync(0xffffffffu, any_resc)) {  // corr is per head: uniform across a warp with this ch
         const uint32_t gp = gi - 1;
         mbar_wait(bar(kBarOFull + (gp & 1)), (gp >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, any_resc)) {  // corr is per head: uniform across a warp with this ch
+        {
 #pragma unroll 1
           for (int g = 0; g < 2; ++g) {
             uint32_t ov[32];
@@ -509,10 +532,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(pfull0 + 8 * buf);
-      } else {
-        fence_proxy_async_cluster();
+      } else {  // (its O^T rescale is done; its P rows travel with the transfer warp)
         __syncwarp();
-        if (lane == 0) mbar_arrive_release_cluster(pfull0 + 8 * buf);
+        if (lane == 0) mbar_arrive_cluster(pfull0 + 8 * buf);
       }
       if (warp == 2) CTRACE(9, gi);
     }
