@@ -23,6 +23,10 @@
 #include "internal.h"
 #include "sm100.cuh"
 
+#ifndef DECODE_EARLY_PF
+#define DECODE_EARLY_PF 1
+#endif
+
 namespace loza {
 
 namespace {
@@ -78,6 +82,9 @@ struct CoopParams {
   int32_t ring;
   int64_t t_cap;
   int32_t n_rows;  // cache rows (an absent sub-block maps here: out of bounds, zero-filled)
+  const uint8_t* kraw;  // contiguous cache rows (L2 prefetch before the dependency wait), or NULL
+  const uint8_t* qraw;  // contiguous Q rows, or NULL
+  int64_t k_sb_bytes, k_st_bytes, q_sb_bytes;
   float scale_log2;
   void* o;
   int64_t o_sb, o_sh;
@@ -246,6 +253,24 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr_smem;
+#if DECODE_EARLY_PF
+  // Under programmatic dependent launch this CTA may start while the previous kernel still runs. Before
+  // waiting for it, pull the first pair tile's cache rows (both sub-blocks: this CTA's K, and V for its
+  // dims) and this CTA's Q half into L2: hints only (seq_lens read here may be stale; nothing is consumed
+  // before the wait), so the first loads after the wait hit L2 instead of paying the HBM latency.
+  if (warp == 0 && lane == 0 && p.kraw) {
+    const SeqTiles s0 = seq_tiles(p, bi);
+    for (int j = 0; j < 2; ++j) {
+      const int32_t k0 = sub_k0(s0, j);
+      if (k0 < 0) continue;
+      const int32_t row = kv_row(p, k0);
+      int32_t nr = p.n_rows - row;
+      nr = nr > 128 ? 128 : nr;
+      if (nr > 0) bulk_prefetch_l2(p.kraw + bi * p.k_sb_bytes + row * p.k_st_bytes, (uint32_t)(nr * p.k_st_bytes));
+    }
+    if (p.qraw) bulk_prefetch_l2(p.qraw + bi * p.q_sb_bytes + rank * 32 * kDqk * 2, 32 * kDqk * 2);
+  }
+#endif
   asm volatile("griddepcontrol.wait;" ::: "memory");  // inputs of the previous kernel are visible from here
   if (p.trace && threadIdx.x == 0) {
     unsigned long long g;
@@ -653,6 +678,11 @@ cudaError_t launch_decode_coop(const AttnProblem& a, cudaStream_t st) {
   p.ring = a.ring;
   p.t_cap = a.ring ? (int64_t)0x7FFFFFFF : a.n_kv;
   p.n_rows = (int32_t)a.n_kv;
+  p.kraw = a.kv.seg[0].k_st == kDqk ? reinterpret_cast<const uint8_t*>(a.kv.seg[0].k) : nullptr;
+  p.k_sb_bytes = a.kv.seg[0].k_sb * 2;
+  p.k_st_bytes = a.kv.seg[0].k_st * 2;
+  p.qraw = a.q_sh == kDqk ? reinterpret_cast<const uint8_t*>(a.q) : nullptr;
+  p.q_sb_bytes = a.q_sb * 2;
   p.scale_log2 = a.scale * 1.4426950408889634f;
   p.o = a.o;
   p.o_sb = a.o_sb;
