@@ -379,7 +379,8 @@ def extra_rows(args, q, kv, o, flush, peaks):
     out["backward_ssa_8k"] = {
         "ms": bw_ms, "tflops": bw_flop / (bw_ms * 1e-3) / 1e12,
         "frac_tensor": bw_flop / (bw_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
-        "kernel": "FFMA first version (attn_bwd_simt.cu): correctness path, tensor-core version next",
+        "kernel": "FFMA, tiled (attn_bwd_simt.cu: CTA-shared staged rows, 16-B staging, dimension pairs); "
+                  "tensor-core version next",
         "algorithmic_flop": bw_flop}
     del of, osp, dh, oh
     # non-absorbed (MHA-form) SSA prefill: per-head K/V (192 / 128) at the headline's 32K

@@ -7,6 +7,7 @@
 // dK_j and dV_j over the rows that attend key j (no atomics: deterministic). Dims are spread over the
 // lanes (lane + 32 c), dot products are warp-reduced. The allowed sets are the closed form of the block
 // selection (select_blocks.cu): sink blocks [0, s) and local blocks [max(s, QB - l + 1), QB], causal j <= p.
+// Tiled variants below share staged rows across a CTA's warps (used when H % 8 == 0 and b % 16 == 0).
 // Tensor-core version: a later round.
 #include <math.h>
 
@@ -203,6 +204,245 @@ __global__ void __launch_bounds__(256) bwd_keys_kernel(BwdParams p) {
   }
 }
 
+// ---------------------------------------------------------------- tiled variants (H % 8 == 0, b % 16 == 0)
+// The kernels above re-read every key row per query row and every query row per key. Here a CTA shares
+// staged rows between its 8 warps, rows are staged with 16-byte vector loads (converted to fp32 in shared
+// memory), and each lane owns dimension PAIRS d = 2 lane + 64 c (8-byte shared reads, two FMAs per read):
+//  * rows: a CTA = the 8 heads h0 .. h0 + 7 of one token (identical key sets); keys are staged kKB at a time
+//    and consumed by all 8 warps (one query row each).
+//  * keys: a CTA = kKT = 16 keys of one b-block (identical attending row sets up to the per-key causal
+//    bound); query rows (q, dO, LSE, D) are staged kRB at a time; each warp owns 2 keys (K/V and the dK/dV
+//    accumulators in registers). Deterministic (no atomics).
+constexpr int kKB = 8, kKT = 16, kRB = 8;
+constexpr int kPQ = 9, kPV = 8;  // dimension pairs per lane: d_qk <= 576, d_v <= 512
+
+// stage element range [0, d) of a row at `src + off` (elements) into dst[0, d) fp32; `tid`/`nth` split the
+// work; vector path when the row start is 16-byte aligned and d spans whole 16-byte vectors
+__device__ __forceinline__ void stage_row(float* dst, const void* src, int64_t off, int d, int bf16, int tid,
+                                          int nth) {
+  const int esz = bf16 ? 2 : 4, per = 16 / esz;
+  const uint8_t* a = reinterpret_cast<const uint8_t*>(src) + off * esz;
+  if (((reinterpret_cast<uintptr_t>(a) & 15) == 0) && d % per == 0) {
+    for (int v = tid; v < d / per; v += nth) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(a) + v);
+      if (bf16) {
+        float4 lo, hi;
+        lo.x = __uint_as_float(x.x << 16); lo.y = __uint_as_float(x.x & 0xFFFF0000u);
+        lo.z = __uint_as_float(x.y << 16); lo.w = __uint_as_float(x.y & 0xFFFF0000u);
+        hi.x = __uint_as_float(x.z << 16); hi.y = __uint_as_float(x.z & 0xFFFF0000u);
+        hi.z = __uint_as_float(x.w << 16); hi.w = __uint_as_float(x.w & 0xFFFF0000u);
+        reinterpret_cast<float4*>(dst)[2 * v] = lo;
+        reinterpret_cast<float4*>(dst)[2 * v + 1] = hi;
+      } else {
+        reinterpret_cast<uint4*>(dst)[v] = x;
+      }
+    }
+  } else {
+    for (int e = tid; e < d; e += nth) dst[e] = ldf(src, off + e, bf16);
+  }
+}
+__device__ __forceinline__ float2 ld2(const float* p) { return *reinterpret_cast<const float2*>(p); }
+
+__global__ void __launch_bounds__(256) bwd_rows_tiled_kernel(BwdParams p, int v_alias) {
+  extern __shared__ float sm[];  // [kKB][kstride]: d_qk (+ d_v unless V aliases K's first d_v columns)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)p.n_q * p.heads;
+  const int64_t w0 = (int64_t)blockIdx.x * 8;
+  const int64_t bi = w0 / rows, r0 = w0 - bi * rows;
+  const int64_t t = r0 / p.heads, h = r0 - t * p.heads + warp;
+  const int64_t pos = p.q_start + t;
+  const int kstride = p.d_qk + (v_alias ? 0 : p.d_v);
+  float2 qv[kPQ], dq[kPQ], dov[kPV];
+  const int64_t qo = bi * p.q_sb + t * p.q_st + h * p.q_sh;
+  const int64_t oo = bi * p.o_sb + t * p.o_st + h * p.o_sh;
+  float Dp = 0.f;
+#pragma unroll
+  for (int c = 0; c < kPQ; ++c) {
+    const int d = 2 * lane + 64 * c;
+    qv[c] = d < p.d_qk ? make_float2(ldf(p.q, qo + d, p.in_bf16), ldf(p.q, qo + d + 1, p.in_bf16)) : make_float2(0.f, 0.f);
+    dq[c] = make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int c = 0; c < kPV; ++c) {
+    const int d = 2 * lane + 64 * c;
+    if (d < p.d_v) {
+      dov[c] = make_float2(ldf(p.dout, oo + d, p.out_bf16), ldf(p.dout, oo + d + 1, p.out_bf16));
+      Dp = fmaf(dov[c].x, ldf(p.o, oo + d, p.out_bf16), fmaf(dov[c].y, ldf(p.o, oo + d + 1, p.out_bf16), Dp));
+    } else {
+      dov[c] = make_float2(0.f, 0.f);
+    }
+  }
+  const float D = warp_sum(Dp);
+  const float lse = p.lse[(bi * p.heads + h) * p.n_q + t];
+  int64_t ja[2], jb[2];
+  key_ranges(p, pos, ja[0], jb[0], ja[1], jb[1]);
+  const int64_t na = jb[0] - ja[0], nk = na + (jb[1] - ja[1]);
+  for (int64_t c0 = 0; c0 < nk; c0 += kKB) {
+    const int nc = (int)(nk - c0 < kKB ? nk - c0 : kKB);
+    // 32 threads per staged key row (warp kk stages key kk)
+    if (warp < nc) {
+      const int64_t f = c0 + warp, j = f < na ? ja[0] + f : ja[1] + (f - na);
+      stage_row(sm + warp * kstride, p.k, bi * p.k_sb + j * p.k_st, p.d_qk, p.in_bf16, lane, 32);
+      if (!v_alias) stage_row(sm + warp * kstride + p.d_qk, p.v, bi * p.v_sb + j * p.v_st, p.d_v, p.in_bf16, lane, 32);
+    }
+    __syncthreads();
+    for (int kk = 0; kk < nc; ++kk) {
+      const float* kr = sm + kk * kstride;
+      const float* vr = v_alias ? kr : kr + p.d_qk;
+      float2 k2[kPQ];
+      float zp = 0.f, dpp = 0.f;
+#pragma unroll
+      for (int c = 0; c < kPQ; ++c) {
+        const int d = 2 * lane + 64 * c;
+        k2[c] = d < p.d_qk ? ld2(kr + d) : make_float2(0.f, 0.f);
+        zp = fmaf(qv[c].x, k2[c].x, fmaf(qv[c].y, k2[c].y, zp));
+      }
+#pragma unroll
+      for (int c = 0; c < kPV; ++c) {
+        const int d = 2 * lane + 64 * c;
+        if (d < p.d_v) {
+          const float2 v2 = ld2(vr + d);
+          dpp = fmaf(dov[c].x, v2.x, fmaf(dov[c].y, v2.y, dpp));
+        }
+      }
+      const float z = warp_sum(zp) * p.scale, dP = warp_sum(dpp);
+      const float P = expf(z - lse);
+      const float dS = P * (dP - D) * p.scale;
+#pragma unroll
+      for (int c = 0; c < kPQ; ++c) {
+        dq[c].x = fmaf(dS, k2[c].x, dq[c].x);
+        dq[c].y = fmaf(dS, k2[c].y, dq[c].y);
+      }
+    }
+    __syncthreads();
+  }
+  float* dqo = p.dq + ((bi * p.n_q + t) * p.heads + h) * p.d_qk;
+#pragma unroll
+  for (int c = 0; c < kPQ; ++c) {
+    const int d = 2 * lane + 64 * c;
+    if (d < p.d_qk) *reinterpret_cast<float2*>(dqo + d) = dq[c];
+  }
+  if (lane == 0) p.D[bi * rows + r0 + warp] = D;
+}
+
+__global__ void __launch_bounds__(256) bwd_keys_tiled_kernel(BwdParams p) {
+  extern __shared__ float sm[];  // [kRB][d_qk + d_v] rows (q, dO), then lse[kRB], D[kRB]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tiles = (p.n_kv + kKT - 1) / kKT;
+  const int64_t bi = blockIdx.x / tiles, j0 = (blockIdx.x - bi * tiles) * kKT;
+  const int rstride = p.d_qk + p.d_v;
+  float* lse_s = sm + kRB * rstride;
+  float* D_s = lse_s + kRB;
+  int64_t jk[2];
+  bool kvalid[2];
+  float2 kv[2][kPQ], vv[2][kPV], dk[2][kPQ], dv[2][kPV];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    jk[e] = j0 + 2 * warp + e;
+    kvalid[e] = jk[e] < p.n_kv;
+    const int64_t jj = kvalid[e] ? jk[e] : 0;
+    const int64_t ko = bi * p.k_sb + jj * p.k_st, vo = bi * p.v_sb + jj * p.v_st;
+#pragma unroll
+    for (int c = 0; c < kPQ; ++c) {
+      const int d = 2 * lane + 64 * c;
+      kv[e][c] = d < p.d_qk ? make_float2(ldf(p.k, ko + d, p.in_bf16), ldf(p.k, ko + d + 1, p.in_bf16))
+                            : make_float2(0.f, 0.f);
+      dk[e][c] = make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int c = 0; c < kPV; ++c) {
+      const int d = 2 * lane + 64 * c;
+      vv[e][c] = d < p.d_v ? make_float2(ldf(p.v, vo + d, p.in_bf16), ldf(p.v, vo + d + 1, p.in_bf16))
+                           : make_float2(0.f, 0.f);
+      dv[e][c] = make_float2(0.f, 0.f);
+    }
+  }
+  // rows attending the tile's keys: causal pos >= j (per key below); SSA local block kb: blocks kb .. kb + l - 1
+  int64_t p0 = p.causal ? j0 : 0, p1 = p.q_start + p.n_q;
+  if (p.sparse) {
+    const int64_t kb = j0 / p.b;
+    if (kb >= p.s) {
+      const int64_t pe = (kb + p.l) * (int64_t)p.b;
+      if (pe < p1) p1 = pe;
+    }
+  }
+  if (p0 < p.q_start) p0 = p.q_start;
+  const int32_t nrow = p1 > p0 ? (int32_t)((p1 - p0) * p.heads) : 0;
+  const int64_t rows = (int64_t)p.n_q * p.heads;
+  const int32_t tq0 = (int32_t)(p0 - p.q_start), H = p.heads;
+  for (int32_t rc = 0; rc < nrow; rc += kRB) {
+    const int nr = nrow - rc < kRB ? nrow - rc : kRB;
+    if (warp < nr) {  // warp rr stages row rr (q then dO)
+      const int32_t ri = rc + warp, t = tq0 + ri / H, h = ri - (ri / H) * H;
+      stage_row(sm + warp * rstride, p.q, bi * p.q_sb + (int64_t)t * p.q_st + (int64_t)h * p.q_sh, p.d_qk, p.in_bf16,
+                lane, 32);
+      stage_row(sm + warp * rstride + p.d_qk, p.dout, bi * p.o_sb + (int64_t)t * p.o_st + (int64_t)h * p.o_sh, p.d_v,
+                p.out_bf16, lane, 32);
+      if (lane == 0) {
+        lse_s[warp] = p.lse[(bi * p.heads + h) * p.n_q + t];
+        D_s[warp] = p.D[bi * rows + (int64_t)t * p.heads + h];
+      }
+    }
+    __syncthreads();
+    for (int rr = 0; rr < nr; ++rr) {
+      const int64_t pos = p0 + (rc + rr) / H;
+      const float* qr = sm + rr * rstride;
+      const float* dor = qr + p.d_qk;
+      float2 q2[kPQ], o2[kPV];
+#pragma unroll
+      for (int c = 0; c < kPQ; ++c) {
+        const int d = 2 * lane + 64 * c;
+        q2[c] = d < p.d_qk ? ld2(qr + d) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int c = 0; c < kPV; ++c) {
+        const int d = 2 * lane + 64 * c;
+        o2[c] = d < p.d_v ? ld2(dor + d) : make_float2(0.f, 0.f);
+      }
+      const float lse = lse_s[rr], Dr = D_s[rr];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (!kvalid[e] || (p.causal && pos < jk[e])) continue;  // warp-uniform
+        float zp = 0.f, dpp = 0.f;
+#pragma unroll
+        for (int c = 0; c < kPQ; ++c) zp = fmaf(q2[c].x, kv[e][c].x, fmaf(q2[c].y, kv[e][c].y, zp));
+#pragma unroll
+        for (int c = 0; c < kPV; ++c) dpp = fmaf(o2[c].x, vv[e][c].x, fmaf(o2[c].y, vv[e][c].y, dpp));
+        const float z = warp_sum(zp) * p.scale, dP = warp_sum(dpp);
+        const float P = expf(z - lse);
+        const float dS = P * (dP - Dr) * p.scale;
+#pragma unroll
+        for (int c = 0; c < kPQ; ++c) {
+          dk[e][c].x = fmaf(dS, q2[c].x, dk[e][c].x);
+          dk[e][c].y = fmaf(dS, q2[c].y, dk[e][c].y);
+        }
+#pragma unroll
+        for (int c = 0; c < kPV; ++c) {
+          dv[e][c].x = fmaf(P, o2[c].x, dv[e][c].x);
+          dv[e][c].y = fmaf(P, o2[c].y, dv[e][c].y);
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    if (!kvalid[e]) continue;
+    float* dko = p.dk + (bi * p.n_kv + jk[e]) * p.d_qk;
+    float* dvo = p.dv + (bi * p.n_kv + jk[e]) * p.d_v;
+#pragma unroll
+    for (int c = 0; c < kPQ; ++c) {
+      const int d = 2 * lane + 64 * c;
+      if (d < p.d_qk) *reinterpret_cast<float2*>(dko + d) = dk[e][c];
+    }
+#pragma unroll
+    for (int c = 0; c < kPV; ++c) {
+      const int d = 2 * lane + 64 * c;
+      if (d < p.d_v) *reinterpret_cast<float2*>(dvo + d) = dv[e][c];
+    }
+  }
+}
+
 }  // namespace
 
 size_t backward_ws_bytes(const AttnProblem& a) { return sizeof(float) * (size_t)a.batch * a.n_q * a.heads; }
@@ -247,12 +487,32 @@ cudaError_t launch_attn_backward(const AttnProblem& a, const void* dout, float* 
   p.l = a.l;
   p.b = a.b;
   const int64_t rows = (int64_t)a.batch * a.n_q * a.heads, keys = (int64_t)a.batch * a.n_kv;
+  // tiled paths: 8 heads per row CTA, 16-key tiles inside one b-block, dimension pairs (even d)
+  const bool even = a.d_qk % 2 == 0 && a.d_v % 2 == 0;
+  const bool tiled_rows = even && a.heads % 8 == 0, tiled_keys = even && (!a.sparse || a.b % kKT == 0);
+  // V aliases K's first d_v columns (absorbed MLA: one latent row serves both)
+  const int v_alias = p.v == p.k && p.v_st == p.k_st && p.v_sb == p.k_sb && a.d_v <= a.d_qk;
   if (rows > 0) {
-    bwd_rows_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(p);
+    if (tiled_rows) {
+      const size_t smem = sizeof(float) * kKB * (a.d_qk + (v_alias ? 0 : a.d_v));
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(bwd_rows_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      bwd_rows_tiled_kernel<<<(unsigned)(rows / 8), 256, smem, st>>>(p, v_alias);
+    } else {
+      bwd_rows_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(p);
+    }
     count_launch();
   }
   if (keys > 0) {
-    bwd_keys_kernel<<<(unsigned)((keys + 7) / 8), 256, 0, st>>>(p);
+    if (tiled_keys) {
+      const size_t smem = sizeof(float) * (kRB * (a.d_qk + a.d_v) + 2 * kRB);
+      const int64_t tiles = (a.n_kv + kKT - 1) / kKT;
+      bwd_keys_tiled_kernel<<<(unsigned)(a.batch * tiles), 256, smem, st>>>(p);
+    } else {
+      bwd_keys_kernel<<<(unsigned)((keys + 7) / 8), 256, 0, st>>>(p);
+    }
     count_launch();
   }
   return cudaGetLastError();

@@ -97,3 +97,34 @@ def test_backward_q_start_offset():
     assert _norm_err(dq[0].reshape(-1, d).double().cpu().numpy(), rq) <= 1e-4
     assert _norm_err(dk[0].double().cpu().numpy(), rk) <= 1e-4
     assert _norm_err(dv[0].double().cpu().numpy(), rv) <= 1e-4
+
+
+@pytest.mark.parametrize("sparse,causal,q0", [(True, True, 0), (False, True, 0), (False, False, 0), (True, True, 128)])
+def test_backward_tiled_fp32_h8(sparse, causal, q0):
+    """The tiled backward kernels (H % 8 == 0, b % 16 == 0): fp32, H = 8, separate K / V, d 64 / 48, every row
+    and key against the fp64 oracle backward (1e-4 normwise)."""
+    B, n, H, dq_, dv_ = 2, 640, 8, 64, 48
+    pat = (1, 2, 64)
+    qs = Spec(seed=44, tensor_id=TID_Q, batch=B, n=n, heads=H, d=dq_, dtype="f32")
+    ks = Spec(seed=44, tensor_id=TID_K, batch=B, n=n, heads=1, d=dq_, dtype="f32")
+    vs = Spec(seed=44, tensor_id=TID_V, batch=B, n=n, heads=1, d=dv_, dtype="f32")
+    ds = Spec(seed=44, tensor_id=TID_DO, batch=B, n=n, heads=H, d=dv_, dtype="f32")
+    q, k, v, do = (empty_filled(s) for s in (qs, ks, vs, ds))
+    qq, dd = q[:, q0:].contiguous(), do[:, q0:].contiguous()
+    scale = 0.11
+    lse = torch.empty((B, H, n - q0), device="cuda")
+    if sparse:
+        o = loza.ssa_prefill(qq, k, v, pat, scale, d_v=dv_, lse=lse, q_start=q0)
+    else:
+        o = loza.full_attn_ref(qq, k, v, scale, d_v=dv_, lse=lse, causal=causal, q_start=q0)
+    dq, dk, dv = loza.attention_backward(qq, k, o, lse, dd, v=v, pattern=pat if sparse else None, scale=scale,
+                                         d_v=dv_, causal=causal, q_start=q0)
+    torch.cuda.synchronize()
+    for bi in range(B):
+        rq, rk, rv = oracle.attention_backward(gen_rows_f32(qs, (bi * n + q0) * H, (n - q0) * H),
+                                               np.repeat(np.arange(q0, n), H), gen_rows_f32(ks, bi * n, n),
+                                               gen_rows_f32(vs, bi * n, n), gen_rows_f32(ds, (bi * n + q0) * H, (n - q0) * H),
+                                               scale, *pat, sparse=sparse, causal=causal)
+        assert _norm_err(dq[bi].reshape(-1, dq_).double().cpu().numpy(), rq) <= 1e-4
+        assert _norm_err(dk[bi].double().cpu().numpy(), rk) <= 1e-4
+        assert _norm_err(dv[bi].double().cpu().numpy(), rv) <= 1e-4

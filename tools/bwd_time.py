@@ -1,0 +1,19 @@
+"""One SSA backward call at the bench shape (8K, H64, MLA, (1,7,128)) for launch-list timing."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from inputs import TID_DO, TID_K, TID_Q, Spec
+from inputs.device import empty_filled
+from paper_2512_23966_b200 import loza
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+q = empty_filled(Spec(seed=0, tensor_id=TID_Q, batch=1, n=n, heads=64, d=576))
+kv = empty_filled(Spec(seed=0, tensor_id=TID_K, batch=1, n=n, heads=1, d=576))
+do = empty_filled(Spec(seed=0, tensor_id=TID_DO, batch=1, n=n, heads=64, d=512))
+lse = torch.empty((1, 64, n), device="cuda")
+o = loza.ssa_prefill(q, kv, lse=lse)
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+ev[0].record()
+loza.attention_backward(q, kv, o, lse, do)
+ev[1].record()
+torch.cuda.synchronize()
+print(f"backward n={n}: {ev[0].elapsed_time(ev[1]):.1f} ms")
