@@ -737,19 +737,32 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           const uint8_t* dhb = p.d_o_hat ? p.d_o_hat + off : nullptr;
           float gs = 0.f;
           mbar_wait(bar(kBarOfFull), uc & 1);  // this unit's O_full rows, staged in the Q region
+          // d_o_hat chunks are software-pipelined one chunk ahead: the loads of chunk c + 1 are in flight
+          // while chunk c is converted (the TMEM wait's memory clobber would otherwise serialise 4 L2 latencies)
+          const bool dload = row_ok && dhb;
+          uint4 dn[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dn[q] = dload ? ldg_nc_v4(dhb + 16 * q) : make_uint4(0, 0, 0, 0);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t ov[32];
             tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ov);
             uint32_t xw[16], dw[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              dw[4 * q] = dn[q].x; dw[4 * q + 1] = dn[q].y; dw[4 * q + 2] = dn[q].z; dw[4 * q + 3] = dn[q].w;
+            }
+            if (c < 3) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                dn[q] = dload ? ldg_nc_v4(dhb + 64 * (c + 1) + 16 * q) : make_uint4(0, 0, 0, 0);
+            }
             // O_full box m = dims [64 m, +64): row r at m * 8192 + 128 r, 16-B units swizzled by r & 7
             const uint8_t* ofs = smem + kOffQ + (4 * ch + 2 * kh + (c >> 1)) * 8192 + r * 128;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const uint4 x4 = *reinterpret_cast<const uint4*>(ofs + ((((c & 1) * 4 + q) ^ (r & 7)) << 4));
-              const uint4 d4 = (row_ok && dhb) ? ldg_nc_v4(dhb + 64 * c + 16 * q) : make_uint4(0, 0, 0, 0);
               xw[4 * q] = x4.x; xw[4 * q + 1] = x4.y; xw[4 * q + 2] = x4.z; xw[4 * q + 3] = x4.w;
-              dw[4 * q] = d4.x; dw[4 * q + 1] = d4.y; dw[4 * q + 2] = d4.z; dw[4 * q + 3] = d4.w;
             }
             tmem_wait_ld();
             uint32_t wc[16];
