@@ -620,14 +620,14 @@ cudaError_t launch_decode_pair(const AttnProblem& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// pair mode: the key-split pair kernel above; LOZA_DECODE_KERNEL=coop selects the pair-cooperative kernel
-// (attn_tc_decode_coop.cu: correct, -0.7% cold / -4.5% L2-warm per step, not adopted)
+// pair mode: the pair-cooperative kernel (attn_tc_decode_coop.cu) unless LOZA_DECODE_KERNEL=pair selects the
+// key-split pair kernel above (kept for A/B measurement)
 cudaError_t launch_decode_pair_any(const AttnProblem& a, cudaStream_t st) {
-  static const int use_coop = [] {
+  static const int use_split = [] {
     const char* e = getenv("LOZA_DECODE_KERNEL");
-    return e && strcmp(e, "coop") == 0 ? 1 : 0;
+    return e && strcmp(e, "pair") == 0 ? 1 : 0;
   }();
-  return use_coop ? launch_decode_coop(a, st) : launch_decode_pair(a, st);
+  return use_split ? launch_decode_pair(a, st) : launch_decode_coop(a, st);
 }
 
 // pair mode: SSA, 64 heads, whole-tile blocks, and 2 CTAs per sequence fit in one wave
