@@ -443,6 +443,185 @@ __global__ void __launch_bounds__(256) bwd_keys_tiled_kernel(BwdParams p) {
   }
 }
 
+// Key kernel with the query-row staging double-buffered by cp.async (16-byte global -> shared copies that
+// need no registers): rows stay in their input format (bf16 or fp32) in shared memory and are converted at
+// use, so chunk c + 1 streams from HBM while chunk c is computed (Q and dO of a long sequence do not fit
+// in L2: the synchronous staging above exposed the DRAM latency every chunk). Used when every staged row
+// is 16-byte aligned and whole 16-byte vectors long.
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <bool BF16>
+__device__ __forceinline__ float2 raw2(const uint8_t* row, int d) {  // elements d, d + 1 of a staged row
+  if (BF16) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(row + 2 * d);
+    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+  }
+  return *reinterpret_cast<const float2*>(row + 4 * d);
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(256) bwd_keys_async_kernel(BwdParams p) {
+  extern __shared__ __align__(16) uint8_t smb[];  // [2 buf][kRB][q bytes | dO bytes], then lse/D [2][kRB]
+  constexpr int esz = BF16 ? 2 : 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tiles = (p.n_kv + kKT - 1) / kKT;
+  const int64_t bi = blockIdx.x / tiles, j0 = (blockIdx.x - bi * tiles) * kKT;
+  const int qbytes = p.d_qk * esz, rbytes = qbytes + p.d_v * esz;
+  float* lse_s = reinterpret_cast<float*>(smb + 2 * kRB * rbytes);
+  float* D_s = lse_s + 2 * kRB;
+  int64_t jk[2];
+  bool kvalid[2];
+  float2 kv[2][kPQ], vv[2][kPV], dk[2][kPQ], dv[2][kPV];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    jk[e] = j0 + 2 * warp + e;
+    kvalid[e] = jk[e] < p.n_kv;
+    const int64_t jj = kvalid[e] ? jk[e] : 0;
+    const int64_t ko = bi * p.k_sb + jj * p.k_st, vo = bi * p.v_sb + jj * p.v_st;
+#pragma unroll
+    for (int c = 0; c < kPQ; ++c) {
+      const int d = 2 * lane + 64 * c;
+      kv[e][c] = d < p.d_qk ? make_float2(ldf(p.k, ko + d, p.in_bf16), ldf(p.k, ko + d + 1, p.in_bf16))
+                            : make_float2(0.f, 0.f);
+      dk[e][c] = make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int c = 0; c < kPV; ++c) {
+      const int d = 2 * lane + 64 * c;
+      vv[e][c] = d < p.d_v ? make_float2(ldf(p.v, vo + d, p.in_bf16), ldf(p.v, vo + d + 1, p.in_bf16))
+                           : make_float2(0.f, 0.f);
+      dv[e][c] = make_float2(0.f, 0.f);
+    }
+  }
+  int64_t p0 = p.causal ? j0 : 0, p1 = p.q_start + p.n_q;
+  if (p.sparse) {
+    const int64_t kb = j0 / p.b;
+    if (kb >= p.s) {
+      const int64_t pe = (kb + p.l) * (int64_t)p.b;
+      if (pe < p1) p1 = pe;
+    }
+  }
+  if (p0 < p.q_start) p0 = p.q_start;
+  const int32_t nrow = p1 > p0 ? (int32_t)((p1 - p0) * p.heads) : 0;
+  const int64_t rows = (int64_t)p.n_q * p.heads;
+  const int32_t tq0 = (int32_t)(p0 - p.q_start), H = p.heads;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smb);
+  // issue chunk rc's copies into buffer bb (warp rr copies row rr: q then dO, 16 B per lane per step)
+  auto issue = [&](int32_t rc, int bb) {
+    const int nr = nrow - rc < kRB ? nrow - rc : kRB;
+    if (warp < nr) {
+      const int32_t ri = rc + warp, t = tq0 + ri / H, h = ri - (ri / H) * H;
+      const uint8_t* qg = reinterpret_cast<const uint8_t*>(p.q) + (bi * p.q_sb + (int64_t)t * p.q_st + (int64_t)h * p.q_sh) * esz;
+      const uint8_t* og = reinterpret_cast<const uint8_t*>(p.dout) + (bi * p.o_sb + (int64_t)t * p.o_st + (int64_t)h * p.o_sh) * esz;
+      const uint32_t dst = sbase + (bb * kRB + warp) * rbytes;
+      for (int v = lane; v < qbytes / 16; v += 32) cp_async16(dst + 16 * v, qg + 16 * v);
+      for (int v = lane; v < (rbytes - qbytes) / 16; v += 32) cp_async16(dst + qbytes + 16 * v, og + 16 * v);
+      if (lane == 0) {
+        lse_s[bb * kRB + warp] = p.lse[(bi * p.heads + h) * p.n_q + t];
+        D_s[bb * kRB + warp] = p.D[bi * rows + (int64_t)t * p.heads + h];
+      }
+    }
+    cp_async_commit();
+  };
+  if (nrow > 0) issue(0, 0);
+  int bb = 0;
+  for (int32_t rc = 0; rc < nrow; rc += kRB, bb ^= 1) {
+    const int nr = nrow - rc < kRB ? nrow - rc : kRB;
+    if (rc + kRB < nrow) {
+      issue(rc + kRB, bb ^ 1);  // the other buffer was released by the previous iteration's barrier
+      cp_async_wait1();
+    } else {
+      cp_async_wait0();
+    }
+    __syncthreads();
+    for (int rr = 0; rr < nr; ++rr) {
+      const int64_t pos = p0 + (rc + rr) / H;
+      const uint8_t* qr = smb + (bb * kRB + rr) * rbytes;
+      const uint8_t* dor = qr + qbytes;
+      float2 q2[kPQ], o2[kPV];
+#pragma unroll
+      for (int c = 0; c < kPQ; ++c) {
+        const int d = 2 * lane + 64 * c;
+        q2[c] = d < p.d_qk ? raw2<BF16>(qr, d) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int c = 0; c < kPV; ++c) {
+        const int d = 2 * lane + 64 * c;
+        o2[c] = d < p.d_v ? raw2<BF16>(dor, d) : make_float2(0.f, 0.f);
+      }
+      const float lse = lse_s[bb * kRB + rr], Dr = D_s[bb * kRB + rr];
+      // both keys in one straight-line body (masked, not branched) so their dependency chains interleave;
+      // each dot product in two partial sums
+      float za[2] = {0.f, 0.f}, zb[2] = {0.f, 0.f}, pa[2] = {0.f, 0.f}, pb[2] = {0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < kPQ; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          za[e] = fmaf(q2[c].x, kv[e][c].x, za[e]);
+          zb[e] = fmaf(q2[c].y, kv[e][c].y, zb[e]);
+        }
+#pragma unroll
+      for (int c = 0; c < kPV; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          pa[e] = fmaf(o2[c].x, vv[e][c].x, pa[e]);
+          pb[e] = fmaf(o2[c].y, vv[e][c].y, pb[e]);
+        }
+      float z[2] = {za[0] + zb[0], za[1] + zb[1]}, dP[2] = {pa[0] + pb[0], pa[1] + pb[1]};
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          z[e] += __shfl_xor_sync(0xffffffffu, z[e], o);
+          dP[e] += __shfl_xor_sync(0xffffffffu, dP[e], o);
+        }
+      float P[2], dS[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const bool on = kvalid[e] && !(p.causal && pos < jk[e]);
+        P[e] = on ? expf(z[e] * p.scale - lse) : 0.f;
+        dS[e] = P[e] * (dP[e] - Dr) * p.scale;
+      }
+#pragma unroll
+      for (int c = 0; c < kPQ; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          dk[e][c].x = fmaf(dS[e], q2[c].x, dk[e][c].x);
+          dk[e][c].y = fmaf(dS[e], q2[c].y, dk[e][c].y);
+        }
+#pragma unroll
+      for (int c = 0; c < kPV; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          dv[e][c].x = fmaf(P[e], o2[c].x, dv[e][c].x);
+          dv[e][c].y = fmaf(P[e], o2[c].y, dv[e][c].y);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    if (!kvalid[e]) continue;
+    float* dko = p.dk + (bi * p.n_kv + jk[e]) * p.d_qk;
+    float* dvo = p.dv + (bi * p.n_kv + jk[e]) * p.d_v;
+#pragma unroll
+    for (int c = 0; c < kPQ; ++c) {
+      const int d = 2 * lane + 64 * c;
+      if (d < p.d_qk) *reinterpret_cast<float2*>(dko + d) = dk[e][c];
+    }
+#pragma unroll
+    for (int c = 0; c < kPV; ++c) {
+      const int d = 2 * lane + 64 * c;
+      if (d < p.d_v) *reinterpret_cast<float2*>(dvo + d) = dv[e][c];
+    }
+  }
+}
+
 }  // namespace
 
 size_t backward_ws_bytes(const AttnProblem& a) { return sizeof(float) * (size_t)a.batch * a.n_q * a.heads; }
@@ -506,9 +685,27 @@ cudaError_t launch_attn_backward(const AttnProblem& a, const void* dout, float* 
     count_launch();
   }
   if (keys > 0) {
-    if (tiled_keys) {
+    const int64_t tiles = (a.n_kv + kKT - 1) / kKT;
+    // cp.async staging: every q / dO row 16-byte aligned and whole vectors long (same dtype for q and dO)
+    const int esz = a.in_bf16 ? 2 : 4;
+    auto al = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+    const bool async_ok = tiled_keys && a.in_bf16 == a.out_bf16 && al(a.q) && al(dout) &&
+                          (a.d_qk * esz) % 16 == 0 && (a.d_v * esz) % 16 == 0 && (a.q_sb * esz) % 16 == 0 &&
+                          (a.q_st * esz) % 16 == 0 && (a.q_sh * esz) % 16 == 0 && (a.o_sb * esz) % 16 == 0 &&
+                          (a.o_st * esz) % 16 == 0 && (a.o_sh * esz) % 16 == 0;
+    if (async_ok) {
+      const size_t smem = (size_t)2 * kRB * (a.d_qk + a.d_v) * esz + sizeof(float) * 4 * kRB;
+      cudaError_t e = a.in_bf16 ? cudaFuncSetAttribute(bwd_keys_async_kernel<true>,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                                : cudaFuncSetAttribute(bwd_keys_async_kernel<false>,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      if (a.in_bf16)
+        bwd_keys_async_kernel<true><<<(unsigned)(a.batch * tiles), 256, smem, st>>>(p);
+      else
+        bwd_keys_async_kernel<false><<<(unsigned)(a.batch * tiles), 256, smem, st>>>(p);
+    } else if (tiled_keys) {
       const size_t smem = sizeof(float) * (kRB * (a.d_qk + a.d_v) + 2 * kRB);
-      const int64_t tiles = (a.n_kv + kKT - 1) / kKT;
       bwd_keys_tiled_kernel<<<(unsigned)(a.batch * tiles), 256, smem, st>>>(p);
     } else {
       bwd_keys_kernel<<<(unsigned)((keys + 7) / 8), 256, 0, st>>>(p);
