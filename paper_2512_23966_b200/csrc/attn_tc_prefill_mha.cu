@@ -56,12 +56,16 @@ constexpr int kBarStageFree = kBarOFree + 2;         // [2] (Q buffer = unit par
 constexpr int kBarOLast = kBarStageFree + 2;         // [2] a unit's last PV landed (O buffer parity)
 constexpr int kBarLFull = kBarOLast + 2;             // [2] softmax -> epilogue: row sums and maxima (local)
 constexpr int kBarLFree = kBarLFull + 2;             // [2] epilogue has read them (local)
-constexpr int kNumBars = kBarLFree + 2;
+constexpr int kUSlots = 4;                           // decoded-unit ring (scheduler warp -> every role)
+constexpr int kBarUFull = kBarLFree + 2;             // [kUSlots]
+constexpr int kBarUEmpty = kBarUFull + kUSlots;      // [kUSlots]
+constexpr int kNumBars = kBarUEmpty + kUSlots;
 constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
 constexpr int kOffPub = kOffTmemPtr + 4;
 constexpr int kOffRed = (kOffPub + 8 + 15) & ~15;
 constexpr int kOffLs = kOffRed + 2 * 2 * 128 * 4;  // float lsum[2 ob][2 ch][128], mrow[2 ob][128]
-constexpr int kSmemUsed = kOffLs + (2 * 2 * 128 + 2 * 128) * 4;
+constexpr int kOffU = kOffLs + (2 * 2 * 128 + 2 * 128) * 4;  // int32 [kUSlots][8]: bi, h, row0, n_sink, loc_begin, n_tiles
+constexpr int kSmemUsed = kOffU + kUSlots * 8 * 4;
 constexpr int kSmemAlloc = kSmemUsed;
 static_assert(kSmemAlloc <= 232448, "smem");
 
@@ -169,6 +173,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       mbar_init(bar(kBarLFull + i), kSoftmaxWarps);
       mbar_init(bar(kBarLFree + i), 4);
     }
+    for (int i = 0; i < kUSlots; ++i) {
+      mbar_init(bar(kBarUFull + i), 1);
+      // consumers: warps 0 and 2 (producers), 4-11 (softmax), 12-15 (epilogue), and the leader's MMA warp
+      mbar_init(bar(kBarUEmpty + i), cluster_ctarank() == 0 ? 15 : 14);
+    }
     mbar_init(bar(kBarPFull), kArrivalsPerPair);
     reinterpret_cast<volatile uint32_t*>(smem + kOffPub)[0] = 0;
     reinterpret_cast<volatile uint32_t*>(smem + kOffPub)[1] = 0;
@@ -189,6 +198,25 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   const int64_t n_iter_total = p.total_units;
   const int64_t ncl = nclusters_x();
   const int64_t cid = cluster_id_x();
+  // the k-th unit of this cluster, decoded by the scheduler warp (warp 3) into the ring; every consumer warp
+  // reads it and releases the slot (no 64-bit / multi-step index math on the MMA and softmax paths)
+  volatile int32_t* uring = reinterpret_cast<volatile int32_t*>(smem + kOffU);
+  auto get_unit = [&](uint32_t k) {
+    const uint32_t slot = k % kUSlots;
+    mbar_wait(bar(kBarUFull + slot), (k / kUSlots) & 1);
+    Unit U;
+    const volatile int32_t* e = uring + 8 * slot;
+    U.bi = e[0];
+    U.h = e[1];
+    U.row0 = e[2];
+    U.n_sink = e[3];
+    U.loc_begin = e[4];
+    U.n_tiles = e[5];
+    U.tok_lo = U.tok_hi = 0;
+    __syncwarp();
+    if (lane == 0) mbar_arrive_local(bar(kBarUEmpty + slot));
+    return U;
+  };
 
   // All roles walk one continuous tile stream across this cluster's units: ring order K(0), K(1), V(0), K(2),
   // V(1), ... with no break at unit boundaries, so S of a unit's first tile is issued before the previous
@@ -223,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     RingPos rp;
     uint32_t uc = 0, g = 0;
     for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
-      const Unit U = make_unit(p, unit_index(p, it));
+      const Unit U = get_unit(uc);
       const uint32_t qb = uc & 1, qpar = ((uc >> 1) & 1) ^ 1;
       if (lane == 0) pub[0] = rp.pos;
       __syncwarp();
@@ -267,8 +295,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       __syncwarp();
       rp.step();
     };
-    for (int64_t it = cid; it < n_iter_total; it += ncl) {
-      const Unit U = make_unit(p, unit_index(p, it));
+    uint32_t vk = 0;
+    for (int64_t it = cid; it < n_iter_total; it += ncl, ++vk) {
+      const Unit U = get_unit(vk);
       for (int i = 0; i < U.n_tiles; ++i) {
         rp.step();  // K(g)
         if (pv_row >= 0) load_v();
@@ -349,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       uint32_t pv_u = 0;
       bool pv_first = false, pv_last = false, have_pv = false;
       for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
-        const Unit U = make_unit(p, unit_index(p, it));
+        const Unit U = get_unit(uc);
         for (int i = 0; i < U.n_tiles; ++i, ++g) {
           issue_s(g, uc, i == 0, i == U.n_tiles - 1);
           if (have_pv) issue_pv(g - 1, pv_u, pv_first, pv_last);
@@ -360,6 +389,25 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         }
       }
       if (have_pv) issue_pv(g - 1, pv_u, pv_first, pv_last);
+    }
+  } else if (warp == 3) {
+    // ===================================================== unit scheduler (both CTAs)
+    uint32_t k = 0;
+    for (int64_t it = cid; it < n_iter_total; it += ncl, ++k) {
+      const uint32_t slot = k % kUSlots;
+      mbar_wait(bar(kBarUEmpty + slot), ((k / kUSlots) & 1) ^ 1);
+      if (lane == 0) {
+        const Unit U = make_unit(p, unit_index(p, it));
+        volatile int32_t* e = uring + 8 * slot;
+        e[0] = U.bi;
+        e[1] = U.h;
+        e[2] = (int32_t)U.row0;
+        e[3] = U.n_sink;
+        e[4] = U.loc_begin;
+        e[5] = U.n_tiles;
+        mbar_arrive_local(bar(kBarUFull + slot));
+      }
+      __syncwarp();
     }
   }
   } else if (warp >= kEpiWarp0) {
@@ -375,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     const float ln2 = 0.69314718055994531f;
     uint32_t uc = 0, g = 0;
     for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
-      const Unit U = make_unit(p, unit_index(p, it));
+      const Unit U = get_unit(uc);
       const uint32_t ob = uc & 1, par = (uc >> 1) & 1;
       g += U.n_tiles;
       mbar_wait(bar(kBarLFull + ob), par);
@@ -453,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     float* lsm = reinterpret_cast<float*>(smem + kOffLs);
     uint32_t g = 0, uc = 0;
     for (int64_t it = cid; it < n_iter_total; it += ncl, ++uc) {
-      const Unit U = make_unit(p, unit_index(p, it));
+      const Unit U = get_unit(uc);
       const int64_t row_g = U.row0 + 128 * rank + r;  // local query token
       const int64_t my_tok = p.q_start + (row_g < p.n_q ? row_g : p.n_q - 1);
       const uint32_t ob = uc & 1;
