@@ -624,7 +624,8 @@ def run_reference(args):
     line = {"impl": "reference",
             "metric": "SSA prefill tokens/s (B1 H64 n32768 MLA 576/512, (s,l,b)=(1,7,128)); % tensor roofline",
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": N_PREFILL / value * 1e3,  # one full 32K step at the sampled rate
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (counter-based, seed 0)",
             "config": {"workload": "ssa_prefill_32k", "batch": 1, "seq_len": N_PREFILL, "heads": H,
                        "pattern": list(PATTERN)},
