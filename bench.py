@@ -245,7 +245,7 @@ def run_gpu(args):
         # chunk c's upload, chunk c-1's SSA and chunk c-2's download overlap on three streams (PCIe is full
         # duplex), all inside the events the timing helper records on the calling stream. Units are
         # independent, so the output equals the unchunked prefill bit for bit.
-        n_chunks = 16
+        n_chunks = 32  # 16: 53.0 ms, 32: 50.4 ms, 64: 50.5 ms per step (tools/e2e_chunks.py; PCIe-bound, ~55 GB/s each way)
         nc = n_local // n_chunks
         s_h, s_c, s_d = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
         ev_h = [torch.cuda.Event() for _ in range(n_chunks)]
