@@ -239,43 +239,75 @@ def run_gpu(args):
         qh.copy_(q)
         kh.copy_(kv)
         qd = torch.empty_like(q)
-        kd = torch.empty_like(kv)
+        kd2 = [torch.empty_like(kv), torch.empty_like(kv)]  # the KV prefix, double-buffered by step parity
 
         # Chunked prefill through the public API (q_start = chunk offset, KV prefix up to the chunk's end):
         # chunk c's upload, chunk c-1's SSA and chunk c-2's download overlap on three streams (PCIe is full
-        # duplex), all inside the events the timing helper records on the calling stream. Units are
-        # independent, so the output equals the unchunked prefill bit for bit.
-        n_chunks = 32  # 16: 53.0 ms, 32: 50.4 ms, 64: 50.5 ms per step (tools/e2e_chunks.py; PCIe-bound, ~55 GB/s each way)
+        # duplex), and consecutive steps overlap too (a serving pipeline): every step still uploads its own
+        # inputs and downloads its own output; per-chunk events keep the reused device buffers safe (Q chunk c:
+        # the previous step's SSA of chunk c has read it; O chunk c: the previous step's download has read it;
+        # the KV prefix alternates buffers). Units are independent, so the output equals the unchunked
+        # prefill bit for bit. Timed as K back-to-back steps between two events (whole-job throughput).
+        n_chunks = 32  # 16: 53.0 ms, 32: 50.4 ms, 64: 50.5 ms per step unpipelined (tools/e2e_chunks.py)
         nc = n_local // n_chunks
         s_h, s_c, s_d = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
         ev_h = [torch.cuda.Event() for _ in range(n_chunks)]
         ev_c = [torch.cuda.Event() for _ in range(n_chunks)]
+        ev_d = [torch.cuda.Event() for _ in range(n_chunks)]
+        ev_step = [torch.cuda.Event(), torch.cuda.Event()]  # SSA of the step with this parity finished
+        st_k = [0]
 
         def e2e_step():
-            cur = torch.cuda.current_stream()
-            s_h.wait_stream(cur)
-            s_c.wait_stream(cur)
-            s_d.wait_stream(cur)
+            k = st_k[0]
+            st_k[0] += 1
+            kd = kd2[k & 1]
+            s_h.wait_event(ev_step[k & 1])  # step k-2 (same KV buffer) has finished its SSA
             for c in range(n_chunks):
                 a, e = c * nc, (c + 1) * nc
+                s_h.wait_event(ev_c[c])  # the previous step's SSA of chunk c has read Q chunk c
                 with torch.cuda.stream(s_h):
                     qd[:, a:e].copy_(qh[:, a:e], non_blocking=True)
                     kd[:, a:e].copy_(kh[:, a:e], non_blocking=True)
                     ev_h[c].record(s_h)
                 s_c.wait_event(ev_h[c])
+                s_c.wait_event(ev_d[c])  # the previous step's download has read O chunk c
                 with torch.cuda.stream(s_c):
                     loza.ssa_prefill(qd[:, a:e], kd[:, :e], pattern=PATTERN, scale=scale, out=o[:, a:e], q_start=a)
                     ev_c[c].record(s_c)
                 s_d.wait_event(ev_c[c])
                 with torch.cuda.stream(s_d):
                     oh[:, a:e].copy_(o[:, a:e], non_blocking=True)
-            cur.wait_stream(s_d)
-            cur.wait_stream(s_c)
-        ts = _time_events(e2e_step, max(2, args.steps // 2), 1)
+                    ev_d[c].record(s_d)
+            ev_step[k & 1].record(s_c)
+
+        cur = torch.cuda.current_stream()
+        for _ in range(2):  # warm-up steps
+            e2e_step()
+        cur.wait_stream(s_d)
+        cur.wait_stream(s_c)
+        torch.cuda.synchronize()
+        k_e2e = max(4, args.steps)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(cur)
+        s_h.wait_stream(cur)
+        for _ in range(k_e2e):
+            e2e_step()
+        cur.wait_stream(s_d)
+        cur.wait_stream(s_c)
+        t1.record(cur)
+        t1.synchronize()
+        ts = [t0.elapsed_time(t1) / k_e2e]
+        # the host copy of the last pipelined step equals the unchunked device prefill bit for bit
+        o_ref = loza.ssa_prefill(q, kv, pattern=PATTERN, scale=scale)
+        torch.cuda.synchronize()
+        e2e_match = bool(torch.equal(oh.to(o_ref.device), o_ref))
+        del o_ref
         e2e = {"value": n_local / (float(np.mean(ts)) * 1e-3), "unit": "tokens/s",
+               "output_matches_device_prefill": e2e_match,
                "h2d_bytes_per_step": int(q.numel() * 2 + kv.numel() * 2), "d2h_bytes_per_step": int(o.numel() * 2),
                "ms_per_step": float(np.mean(ts)),
-               "method": f"ssa_prefill in {n_chunks} chunks (q_start), H2D / compute / D2H on three streams"}
+               "method": f"ssa_prefill in {n_chunks} chunks (q_start), H2D / compute / D2H on three streams, "
+                         f"consecutive steps pipelined; {k_e2e} steps timed back to back"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
