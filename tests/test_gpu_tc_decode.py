@@ -113,3 +113,24 @@ def test_ssa_decode_bench_config_sampled():
     for bi in (0, 63):
         ref, _ = _oracle_decode(qs, ks, bi, int(sl[bi]), None, sparse=False)
         assert np.abs(of[bi, 0].double().cpu().numpy() - ref).max() <= MAXABS, bi
+
+
+@pytest.mark.parametrize("B", [74, 80])
+def test_ssa_decode_large_batch(B):
+    """B = 74 is the largest batch on the pair kernels (2 CTAs per sequence on 148 SMs); B = 80 runs the
+    flattened split-KV kernel. Ragged seq_lens, sampled sequences against the oracle."""
+    T = 2048
+    pattern = (1, 7, 128)
+    rng = np.random.default_rng(80 + B)
+    seq = [int(x) for x in rng.integers(1, T + 1, B)]
+    seq[0], seq[-1] = 1, T
+    qs = Spec(seed=12, tensor_id=TID_Q, batch=B, n=1, heads=H, d=D_QK)
+    ks = Spec(seed=12, tensor_id=TID_K, batch=B, n=T, heads=1, d=D_QK)
+    q, cache = empty_filled(qs), empty_filled(ks)
+    sl = torch.tensor(seq, dtype=torch.int32, device="cuda")
+    o = loza.ssa_decode(q, cache, sl, pattern=pattern, scale=SCALE)
+    torch.cuda.synchronize()
+    for bi in sorted({0, B - 1, *[int(x) for x in rng.integers(0, B, 6)]}):
+        ref, _ = _oracle_decode(qs, ks, bi, seq[bi], pattern)
+        got = o[bi, 0].double().cpu().numpy()
+        assert np.abs(got - ref).max() <= MAXABS, (bi, seq[bi], np.abs(got - ref).max())
