@@ -93,7 +93,9 @@ loza_status_t ssa_prefill(const loza_attn_args_t* args, loza_pattern_t pattern, 
  * capacity T_cap; seq_lens_dev [B] int32 on the device, 1 <= seq_len <= T_cap
  * (out-of-range values are clamped on the device). q [B,1,H,d_qk] -> o [B,1,H,d_v].
  * ws: loza_workspace_size(LOZA_WS_DECODE, ...) bytes, ZERO-FILLED before its first use (it holds
- * per-sequence split counters that every call leaves at zero again); bf16 path: H == 64. */
+ * per-sequence split counters that every call leaves at zero again); bf16 path: H == 64. Kernel: a CTA
+ * pair per sequence while 2*batch <= SM count (pair-cooperative by default; the environment variable
+ * LOZA_DECODE_KERNEL=pair selects the key-split pair kernel), else a flattened split-KV kernel. */
 loza_status_t ssa_decode(const loza_attn_args_t* args, const int32_t* seq_lens_dev,
                          loza_pattern_t pattern, void* ws, size_t ws_bytes, loza_stream_t stream);
 
