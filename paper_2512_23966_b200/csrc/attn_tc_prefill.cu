@@ -721,13 +721,16 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         uint32_t w[64];
         if constexpr (!calib) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t ov[32];
-            tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ov);
+          for (int c = 0; c < 4; c += 2) {  // two TMEM loads per wait
+            uint32_t ova[32], ovb[32];
+            tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ova);
+            tmem_ld32(taddr + kTmemO + 128 * ch + 32 * (c + 1), ovb);
             tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              w[16 * c + j] = pack_bf16x2(__uint_as_float(ov[2 * j]) * inv, __uint_as_float(ov[2 * j + 1]) * inv);
+            for (int j = 0; j < 16; ++j) {
+              w[16 * c + j] = pack_bf16x2(__uint_as_float(ova[2 * j]) * inv, __uint_as_float(ova[2 * j + 1]) * inv);
+              w[16 * (c + 1) + j] = pack_bf16x2(__uint_as_float(ovb[2 * j]) * inv, __uint_as_float(ovb[2 * j + 1]) * inv);
+            }
           }
         } else {
           // Eq. 3 on this thread's 128 outputs: o_hat = fma(alpha, O, (1 - alpha) O') with O' the fp32 SSA
