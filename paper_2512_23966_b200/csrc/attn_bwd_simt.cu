@@ -8,8 +8,10 @@
 // lanes (lane + 32 c), dot products are warp-reduced. The allowed sets are the closed form of the block
 // selection (select_blocks.cu): sink blocks [0, s) and local blocks [max(s, QB - l + 1), QB], causal j <= p.
 // Tiled variants below share staged rows across a CTA's warps (used when H % 8 == 0 and b % 16 == 0).
-// Tensor-core version: a later round.
+// The absorbed MLA shape in bf16 runs on the tensor cores instead (attn_bwd_mma.cu).
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "internal.h"
 
@@ -624,11 +626,23 @@ __global__ void __launch_bounds__(256) bwd_keys_async_kernel(BwdParams p) {
 
 }  // namespace
 
-size_t backward_ws_bytes(const AttnProblem& a) { return sizeof(float) * (size_t)a.batch * a.n_q * a.heads; }
+static size_t d_bytes(const AttnProblem& a) {
+  return (sizeof(float) * (size_t)a.batch * a.n_q * a.heads + 255) / 256 * 256;
+}
+// D, then (tensor-core path, SSA) the sink-tile partials of attn_bwd_mma.cu
+size_t backward_ws_bytes(const AttnProblem& a) { return d_bytes(a) + backward_mma_part_bytes(a); }
 
 cudaError_t launch_attn_backward(const AttnProblem& a, const void* dout, float* dq, float* dk, float* dv, void* ws,
                                  cudaStream_t st) {
   if (a.d_qk > 32 * kMaxCQ || a.d_v > 32 * kMaxCV) return cudaErrorNotSupported;
+  // the absorbed MLA shape in bf16 runs on the tensor cores (LOZA_BWD_KERNEL=simt forces the FFMA kernels)
+  static const bool force_simt = [] {
+    const char* e = getenv("LOZA_BWD_KERNEL");
+    return e && strcmp(e, "simt") == 0;
+  }();
+  if (!force_simt && backward_mma_eligible(a, dout))
+    return launch_attn_backward_mma(a, dout, dq, dk, dv, reinterpret_cast<float*>(ws),
+                                    reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + d_bytes(a)), st);
   BwdParams p;
   p.q = a.q;
   p.k = a.kv.seg[0].k;

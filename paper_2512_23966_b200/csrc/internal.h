@@ -73,6 +73,12 @@ size_t decode_tc_ws_bytes(const AttnProblem& p);
 bool decode_pair_eligible(const AttnProblem& a, int sms);
 cudaError_t launch_decode_pair(const AttnProblem& a, cudaStream_t st);
 size_t backward_ws_bytes(const AttnProblem& a);
+// tensor-core backward (attn_bwd_mma.cu): bf16, d_qk 576, d_v 512, V = K[:, :512]; D [B][n_q*H] and the
+// sink-tile partials (backward_mma_part_bytes) come from the backward workspace
+bool backward_mma_eligible(const AttnProblem& a, const void* dout);
+size_t backward_mma_part_bytes(const AttnProblem& a);
+cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, float* dq, float* dk, float* dv,
+                                     float* D, float* part, cudaStream_t st);
 cudaError_t launch_attn_backward(const AttnProblem& a, const void* dout, float* dq, float* dk, float* dv, void* ws,
                                  cudaStream_t st);
 cudaError_t launch_ring_append(const void* rows, int64_t r_sb, int64_t r_st, int32_t m, const int32_t* pos0,

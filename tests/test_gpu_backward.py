@@ -128,3 +128,67 @@ def test_backward_tiled_fp32_h8(sparse, causal, q0):
         assert _norm_err(dq[bi].reshape(-1, dq_).double().cpu().numpy(), rq) <= 1e-4
         assert _norm_err(dk[bi].double().cpu().numpy(), rk) <= 1e-4
         assert _norm_err(dv[bi].double().cpu().numpy(), rv) <= 1e-4
+
+
+@pytest.mark.parametrize("sparse,causal,q0,H,n,pat,B,ofwd", [
+    (True, True, 0, 16, 640, (1, 2, 128), 2, False),    # 4 tokens per 64-row tile, 3 sink splits
+    (True, True, 0, 8, 1152, (1, 7, 128), 1, False),    # the paper's pattern, a window boundary inside the sequence
+    (True, True, 128, 8, 512, (1, 2, 128), 1, False),   # chunked prefill (q_start)
+    (True, True, 0, 64, 400, (2, 1, 128), 1, False),    # two sink blocks, H = 64, ragged last block
+    (False, True, 0, 8, 304, None, 1, False),           # full causal, ragged key tile
+    (False, False, 0, 8, 208, None, 1, False),          # bidirectional
+    (True, True, 0, 8, 300, (1, 1, 128), 1, True),      # ragged row tile (2400 rows), 3 sink splits
+    (False, True, 0, 8, 100, None, 1, True),            # ragged rows and keys, one partial key tile set
+])
+def test_backward_mla_mma(sparse, causal, q0, H, n, pat, B, ofwd):
+    """The tensor-core backward (attn_bwd_mma.cu: bf16, 576/512, V = KV[:, :512]) against the fp64 oracle
+    backward, every row and key, bf16 tolerance (2e-2 normwise); deterministic across calls. ofwd: O and LSE
+    from the oracle forward (rounded to bf16 / fp32), for row counts the bf16 forward does not take."""
+    qs = Spec(seed=45, tensor_id=TID_Q, batch=B, n=n, heads=H, d=576)
+    ks = Spec(seed=45, tensor_id=TID_K, batch=B, n=n, heads=1, d=576)
+    ds = Spec(seed=45, tensor_id=TID_DO, batch=B, n=n, heads=H, d=512)
+    q, kv, do = empty_filled(qs), empty_filled(ks), empty_filled(ds)
+    qq, dd = q[:, q0:].contiguous(), do[:, q0:].contiguous()
+    scale = loza.default_scale(576)
+    lse = torch.empty((B, H, n - q0), device="cuda")
+    if ofwd:
+        o = torch.empty((B, n - q0, H, 512), dtype=torch.bfloat16, device="cuda")
+        for bi in range(B):
+            kf = gen_rows_f32(ks, bi * n, n)
+            orow, lrow = oracle.attention_rows(gen_rows_f32(qs, (bi * n + q0) * H, (n - q0) * H),
+                                               np.repeat(np.arange(q0, n), H), kf, kf[:, :512], scale,
+                                               *(pat or (0, 1, 1)), sparse=sparse, causal=causal)
+            o[bi] = torch.from_numpy(orow.reshape(n - q0, H, 512)).to(torch.bfloat16)
+            lse[bi] = torch.from_numpy(lrow.reshape(n - q0, H).T.copy()).float()
+    elif sparse:
+        o = loza.ssa_prefill(qq, kv, pattern=pat, scale=scale, lse=lse, q_start=q0)
+    else:
+        o = loza.full_attn_ref(qq, kv, scale=scale, lse=lse, causal=causal, q_start=q0)
+    run = lambda: loza.attention_backward(qq, kv, o, lse, dd, pattern=pat if sparse else None, scale=scale,  # noqa: E731
+                                          causal=causal, q_start=q0)
+    dq, dk, dv = run()
+    dq2, dk2, dv2 = run()
+    torch.cuda.synchronize()
+    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
+    for bi in range(B):
+        kf = gen_rows_f32(ks, bi * n, n)
+        rq, rk, rv = oracle.attention_backward(gen_rows_f32(qs, (bi * n + q0) * H, (n - q0) * H),
+                                               np.repeat(np.arange(q0, n), H), kf, kf[:, :512],
+                                               gen_rows_f32(ds, (bi * n + q0) * H, (n - q0) * H), scale,
+                                               *(pat or (0, 1, 1)), sparse=sparse, causal=causal)
+        assert _norm_err(dq[bi].reshape(-1, 576).double().cpu().numpy(), rq) <= 2e-2
+        assert _norm_err(dk[bi].double().cpu().numpy(), rk) <= 2e-2
+        assert _norm_err(dv[bi].double().cpu().numpy(), rv) <= 2e-2
+
+
+def test_backward_mla_simt_forced():
+    """LOZA_BWD_KERNEL=simt keeps the FFMA kernels reachable for the MLA shape: the bf16 MLA test through them."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_backward.py") + "::test_backward_mla_bf16_ssa"],
+                       cwd=root, env=dict(os.environ, LOZA_BWD_KERNEL="simt"), capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

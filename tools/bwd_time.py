@@ -11,9 +11,13 @@ kv = empty_filled(Spec(seed=0, tensor_id=TID_K, batch=1, n=n, heads=1, d=576))
 do = empty_filled(Spec(seed=0, tensor_id=TID_DO, batch=1, n=n, heads=64, d=512))
 lse = torch.empty((1, 64, n), device="cuda")
 o = loza.ssa_prefill(q, kv, lse=lse)
-ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-ev[0].record()
-loza.attention_backward(q, kv, o, lse, do)
-ev[1].record()
+loza.attention_backward(q, kv, o, lse, do)  # warm-up (module load, attributes)
 torch.cuda.synchronize()
-print(f"backward n={n}: {ev[0].elapsed_time(ev[1]):.1f} ms")
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+for i in range(3):
+    ev[i].record()
+    loza.attention_backward(q, kv, o, lse, do)
+ev[3].record()
+torch.cuda.synchronize()
+ts = [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
+print(f"backward n={n} ({os.environ.get('LOZA_BWD_KERNEL', 'default')}): " + " ".join(f"{t:.2f}" for t in ts) + " ms")
