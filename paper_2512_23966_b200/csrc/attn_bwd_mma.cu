@@ -239,23 +239,40 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_mma_kernel(MP p) {
     const int buf = it & 1;
     if (it + 1 < ntiles) issue_k(it + 1, buf ^ 1);
     const uint32_t kbase = sb + kROffK + buf * kRKeys * kQRow;
-    float s[2][4] = {}, dp[2][4] = {};
-#pragma unroll 4
-    for (int kk = 0; kk < kDQK / 16; ++kk) {
-      uint32_t a[4], b[4];
+    // two independent chains per 8-key tile (even / odd k steps), summed afterwards
+    float s4[4][4] = {}, d4[4][4] = {};
+#pragma unroll 3
+    for (int kk = 0; kk < kDQK / 16; kk += 2) {
+      uint32_t a[4], b[4], a2[4], b2[4];
       ldsm4(aQ + 32 * kk, a);
       ldsm4(kbase + bK + 32 * kk, b);
-      mma(s[0], a, b[0], b[1]);
-      mma(s[1], a, b[2], b[3]);
+      ldsm4(aQ + 32 * kk + 32, a2);
+      ldsm4(kbase + bK + 32 * kk + 32, b2);
+      mma(s4[0], a, b[0], b[1]);
+      mma(s4[1], a, b[2], b[3]);
+      mma(s4[2], a2, b2[0], b2[1]);
+      mma(s4[3], a2, b2[2], b2[3]);
     }
 #pragma unroll 4
-    for (int kk = 0; kk < kDV / 16; ++kk) {
-      uint32_t a[4], b[4];
+    for (int kk = 0; kk < kDV / 16; kk += 2) {
+      uint32_t a[4], b[4], a2[4], b2[4];
       ldsm4(aO + 32 * kk, a);
       ldsm4(kbase + bK + 32 * kk, b);
-      mma(dp[0], a, b[0], b[1]);
-      mma(dp[1], a, b[2], b[3]);
+      ldsm4(aO + 32 * kk + 32, a2);
+      ldsm4(kbase + bK + 32 * kk + 32, b2);
+      mma(d4[0], a, b[0], b[1]);
+      mma(d4[1], a, b[2], b[3]);
+      mma(d4[2], a2, b2[0], b2[1]);
+      mma(d4[3], a2, b2[2], b2[3]);
     }
+    float s[2][4], dp[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        s[nt][e] = s4[nt][e] + s4[nt + 2][e];
+        dp[nt][e] = d4[nt][e] + d4[nt + 2][e];
+      }
     const int j0 = tile_j0(it), rlo = it < nt0 ? lo[0] : lo[1], rhi = it < nt0 ? hi[0] : hi[1];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
@@ -338,10 +355,32 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_mma_kernel(MP p) {
     cp16(sb + kKOffK + kj * kQRow + 16 * c, p.k + bi * p.k_sb + (int64_t)(v ? j : 0) * p.k_st + 8 * c, v);
   }
   cp_commit();
-  const int nrt = (R1 - R0 + kKRows - 1) / kKRows;
+  // Row tiles in segments. A local (SSA) key tile's rows span <= l query blocks; they are taken block by
+  // block in the order m mod l, so at step sigma every such CTA reads query block m = sigma (mod l): the ~4 l
+  // CTAs whose windows hold a block read it at about the same time (L2 reuse of the Q / dO stream).
+  const int L = p.sparse && !split && kb >= p.s ? p.l : 1;
+  const int m0 = p0 / p.b, m1 = (p1 - 1) / p.b;
+  auto next_seg = [&](int& sig, int& rb, int& re) {  // the first non-empty segment after sig (sig = L: none)
+    while (++sig < L) {
+      if (L == 1) {
+        rb = R0;
+        re = R1;
+      } else {
+        const int m = m0 + ((sig - m0) % L + L) % L;
+        if (m > m1) continue;
+        const int a = m * p.b > p0 ? m * p.b : p0, e = (m + 1) * p.b < p1 ? (m + 1) * p.b : p1;
+        rb = (a - p.q_start) * H;
+        re = (e - p.q_start) * H;
+      }
+      if (rb < re) return;
+    }
+  };
+  auto advance = [&](int& sig, int& rb, int& re) {
+    rb += kKRows;
+    if (rb >= re) next_seg(sig, rb, re);
+  };
   const int rows = p.n_q * H;
-  auto issue = [&](int rt, int bb) {
-    const int rb = R0 + rt * kKRows;
+  auto issue = [&](int rb, int R1, int bb) {
     for (int i = tid; i < kKRows * (kDQK / 8); i += 256) {
       const int ri = i / (kDQK / 8), c = i - ri * (kDQK / 8);
       const bool v = rb + ri < R1;
@@ -378,37 +417,59 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_mma_kernel(MP p) {
   const uint32_t aP = sb + kKOffP + (km + (lane & 15)) * kTRow + (lane >> 4) * 16;
   const uint32_t aD = sb + kKOffDS + (km + (lane & 15)) * kTRow + (lane >> 4) * 16;
   const int trow = (lane & 7) + ((lane >> 3) & 1) * 8, tcol = (lane >> 4) * 8;  // ldmatrix.trans lane address
-  if (nrt > 0) issue(0, 0);
-  for (int rt = 0; rt < nrt; ++rt) {
-    const int bb = rt & 1;
-    if (rt + 1 < nrt) {
-      issue(rt + 1, bb ^ 1);
+  int csig = -1, crb = 0, cre = 0;
+  next_seg(csig, crb, cre);
+  int nsig = csig, nrb = crb, nre = cre;
+  if (csig < L) {
+    issue(crb, cre, 0);
+    advance(nsig, nrb, nre);
+  }
+  for (int bb = 0; csig < L; bb ^= 1) {
+    if (nsig < L) {
+      issue(nrb, nre, bb ^ 1);
       cp_wait<1>();
     } else {
       cp_wait<0>();
     }
     __syncthreads();
     const uint32_t qbase = sb + kKOffQ + bb * kKRows * kQRow, obase = sb + kKOffDO + bb * kKRows * kORow;
-    float st[4] = {}, dpt[4] = {};
+    // four independent accumulator chains per product (the k steps mod 4), summed afterwards
+    float st4[4][4] = {}, dp4[4][4] = {};
 #pragma unroll 3
-    for (int k2 = 0; k2 < kDQK / 32; ++k2) {
-      uint32_t a[4], b[4];
+    for (int k2 = 0; k2 < kDQK / 32; k2 += 2) {
+      uint32_t a[4], b[4], b2[4];
       ldsm4(qbase + bQ + 64 * k2, b);
+      ldsm4(qbase + bQ + 64 * k2 + 64, b2);
       ldsm4(aK + 64 * k2, a);
-      mma(st, a, b[0], b[1]);
+      mma(st4[0], a, b[0], b[1]);
       ldsm4(aK + 64 * k2 + 32, a);
-      mma(st, a, b[2], b[3]);
+      mma(st4[1], a, b[2], b[3]);
+      ldsm4(aK + 64 * k2 + 64, a);
+      mma(st4[2], a, b2[0], b2[1]);
+      ldsm4(aK + 64 * k2 + 96, a);
+      mma(st4[3], a, b2[2], b2[3]);
     }
 #pragma unroll 4
-    for (int k2 = 0; k2 < kDV / 32; ++k2) {
-      uint32_t a[4], b[4];
+    for (int k2 = 0; k2 < kDV / 32; k2 += 2) {
+      uint32_t a[4], b[4], b2[4];
       ldsm4(obase + bO + 64 * k2, b);
+      ldsm4(obase + bO + 64 * k2 + 64, b2);
       ldsm4(aK + 64 * k2, a);
-      mma(dpt, a, b[0], b[1]);
+      mma(dp4[0], a, b[0], b[1]);
       ldsm4(aK + 64 * k2 + 32, a);
-      mma(dpt, a, b[2], b[3]);
+      mma(dp4[1], a, b[2], b[3]);
+      ldsm4(aK + 64 * k2 + 64, a);
+      mma(dp4[2], a, b2[0], b2[1]);
+      ldsm4(aK + 64 * k2 + 96, a);
+      mma(dp4[3], a, b2[2], b2[3]);
     }
-    const int rb = R0 + rt * kKRows;
+    float st[4], dpt[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      st[e] = (st4[0][e] + st4[1][e]) + (st4[2][e] + st4[3][e]);
+      dpt[e] = (dp4[0][e] + dp4[1][e]) + (dp4[2][e] + dp4[3][e]);
+    }
+    const int rb = crb, R1 = cre;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       float pv[2], dsv[2];
@@ -452,6 +513,10 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_mma_kernel(MP p) {
       }
     }
     __syncthreads();  // buffers bb and the P / dS tiles free
+    csig = nsig;
+    crb = nrb;
+    cre = nre;
+    if (nsig < L) advance(nsig, nrb, nre);
   }
   cp_wait<0>();  // (no row tiles: the K tile copy)
   // C fragment: keys km + g (+8), columns 8 n + 2 t4 of [dK | dV]
