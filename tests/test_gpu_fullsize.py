@@ -1,5 +1,5 @@
 """Parity at the BASELINE.json sizes the bench times, on sampled outputs the fp64 oracle computes one by one
-(DESIGN.md §3): blend and the fused calibration forward at 8K (configs[2]), the ring-cache decode at position
+(DESIGN.md §3): blend, the fused calibration forward and the backward at 8K (configs[2]), the ring-cache decode at position
 1M (configs[3]), and the sequence-parallel prefill at 8 virtual ranks (the bench's largest topology).
 """
 import numpy as np
@@ -127,3 +127,42 @@ def test_mha_prefill_32k_sampled():
         qr = gen_rows_f32(specs[0], t * Hm + h, 1)
         ref, _ = oracle.attend(qr, kk[sel], vv[sel], scale)
         assert np.abs(o[0, t, h].double().cpu().numpy() - ref[0]).max() <= 2e-2, (t, h)
+
+
+def test_backward_8k_sampled():
+    """Attention backward (the tensor-core kernels) at the bench shape: B1, 8192 tokens, H64,
+    MLA 576/512, (1,7,128), bf16, in the bench's launch configuration.
+    - dQ of sampled (token, head) rows against the oracle backward over those rows (a dQ row depends on its
+      own row only);
+    - dK, dV of the last 8 keys against the oracle backward over the 512 rows that attend them (causal);
+    - at full size, two identities of the gradient: sum_j dS_rj = 0 for every row (so sum_j dK_j = 0) and
+      sum_j P_rj = 1 (so sum_j dV_j = sum_r dO_r). They cover every key, the sink tiles and their split
+      reduction included. Tolerance: each dK_j / dV_j may carry a bf16-operand rounding error of relative
+      size 2^-7 in an independent direction, so the sums may deviate by 2^-7 * sqrt(sum_j ||.||^2); a dropped
+      term or a lost split is orders of magnitude larger."""
+    n = 8192
+    qs = Spec(seed=56, tensor_id=TID_Q, batch=1, n=n, heads=H, d=D_QK)
+    ks = Spec(seed=56, tensor_id=TID_K, batch=1, n=n, heads=1, d=D_QK)
+    ds = Spec(seed=56, tensor_id=TID_DO, batch=1, n=n, heads=H, d=D_V)
+    q, kv, do = empty_filled(qs), empty_filled(ks), empty_filled(ds)
+    scale = loza.default_scale(D_QK)
+    lse = torch.empty((1, H, n), device="cuda")
+    o = loza.ssa_prefill(q, kv, pattern=PAT, scale=scale, lse=lse)
+    dq, dk, dv = loza.attention_backward(q, kv, o, lse, do, pattern=PAT, scale=scale)
+    torch.cuda.synchronize()
+    kf = gen_rows_f32(ks, 0, n)
+    samples = [(0, 0), (127, 9), (128, 63), (1000, 1), (1023, 40), (1024, 7), (5000, 33), (8191, 62)]
+    qr = np.concatenate([gen_rows_f32(qs, t * H + h, 1) for t, h in samples])
+    dr = np.concatenate([gen_rows_f32(ds, t * H + h, 1) for t, h in samples])
+    rq, _, _ = oracle.attention_backward(qr, np.array([t for t, _ in samples]), kf, kf[:, :D_V], dr, scale, *PAT)
+    got = np.stack([dq[0, t, h].double().cpu().numpy() for t, h in samples])
+    assert np.abs(got - rq).max() / np.abs(rq).max() <= 2e-2
+    t0 = n - 8
+    _, rk, rv = oracle.attention_backward(gen_rows_f32(qs, t0 * H, 8 * H), np.repeat(np.arange(t0, n), H), kf,
+                                          kf[:, :D_V], gen_rows_f32(ds, t0 * H, 8 * H), scale, *PAT)
+    assert np.abs(dk[0, t0:].double().cpu().numpy() - rk[t0:]).max() / np.abs(rk[t0:]).max() <= 2e-2
+    assert np.abs(dv[0, t0:].double().cpu().numpy() - rv[t0:]).max() / np.abs(rv[t0:]).max() <= 2e-2
+    dk64, dv64 = dk[0].double(), dv[0].double()
+    assert dk64.sum(0).norm().item() <= 2.0 ** -7 * dk64.pow(2).sum().sqrt().item()
+    sd = do[0].double().reshape(-1, D_V).sum(0)
+    assert (dv64.sum(0) - sd).norm().item() <= 2.0 ** -7 * dv64.pow(2).sum().sqrt().item()
