@@ -49,7 +49,9 @@ constexpr int kKOffP = kKOffDO + 2 * kKRows * kORow;
 constexpr int kKOffDS = kKOffP + kKKeys * kTRow;
 constexpr int kKOffL = kKOffDS + kKKeys * kTRow;
 constexpr int kKOffD = kKOffL + 2 * kKRows * 4;
-constexpr int kKSmem = kKOffD + 2 * kKRows * 4;
+constexpr int kKOffPos = kKOffD + 2 * kKRows * 4;  // int [2][32]: the row's position
+constexpr int kKOffLb = kKOffPos + 2 * kKRows * 4;  // int [2][32]: its first local block pos / b - l + 1
+constexpr int kKSmem = kKOffLb + 2 * kKRows * 4;
 static_assert(kRSmem <= 227 * 1024 && kKSmem <= 227 * 1024, "shared memory");
 
 struct MP {
@@ -68,7 +70,16 @@ struct MP {
   float scale, sl2;
   int32_t sparse, causal, s, l, b;
   int32_t nsplit, n_sink;
+  uint32_t h_m, h_p;  // n / heads = (n * h_m) >> h_p, exact for n < 2^31
 };
+
+__host__ void fastdiv_init(uint32_t d, uint32_t& m, uint32_t& sh) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  sh = 31 + l;
+  m = (uint32_t)(((1ull << sh) + d - 1) / d);
+}
+__device__ __forceinline__ int div_h(const MP& p, int n) { return (int)(((uint64_t)(uint32_t)n * p.h_m) >> p.h_p); }
 
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
@@ -108,14 +119,9 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 }
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v)); }
 
-// the selection rule of attn_bwd_simt.cu's key_ranges as a predicate (query at absolute position pos, key j)
-__device__ __forceinline__ bool allowed(const MP& p, int pos, int j) {
-  if (j >= p.n_kv) return false;
-  if (p.causal && j > pos) return false;
-  if (!p.sparse) return true;
-  const int kb = j / p.b;
-  return kb < p.s || kb >= pos / p.b - p.l + 1;
-}
+// The selection rule of attn_bwd_simt.cu's key_ranges as a predicate, for the query at position pos and key j:
+//   j < n_kv  and  (not causal or j <= pos)  and  (dense or j / b < s or j / b >= pos / b - l + 1),
+// evaluated below with the key block hoisted per tile and the row terms precomputed.
 __device__ __forceinline__ int last_key(const MP& p, int pos) {
   return p.causal ? (pos + 1 < p.n_kv ? pos + 1 : p.n_kv) : p.n_kv;
 }
@@ -135,13 +141,13 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_mma_kernel(MP p) {
   for (int i = tid; i < kRRows * (kDQK / 8); i += 256) {
     const int ri = i / (kDQK / 8), c = i - ri * (kDQK / 8);
     const bool v = ri < nr;
-    const int r = v ? r0 + ri : 0, t = r / H, h = r - t * H;
+    const int r = v ? r0 + ri : 0, t = div_h(p, r), h = r - t * H;
     cp16(sb + kROffQ + ri * kQRow + 16 * c, p.q + bi * p.q_sb + (int64_t)t * p.q_st + (int64_t)h * p.q_sh + 8 * c, v);
   }
   for (int i = tid; i < kRRows * (kDV / 8); i += 256) {
     const int ri = i / (kDV / 8), c = i - ri * (kDV / 8);
     const bool v = ri < nr;
-    const int r = v ? r0 + ri : 0, t = r / H, h = r - t * H;
+    const int r = v ? r0 + ri : 0, t = div_h(p, r), h = r - t * H;
     cp16(sb + kROffDO + ri * kORow + 16 * c, p.dout + bi * p.o_sb + (int64_t)t * p.o_st + (int64_t)h * p.o_sh + 8 * c, v);
   }
   cp_commit();
@@ -216,14 +222,15 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_mma_kernel(MP p) {
   __syncthreads();
   const int mrow = 16 * (warp & 3), ncol = 16 * (warp >> 2), dh = 288 * (warp >> 2);
   // this thread's two C-fragment rows
-  int posr[2];
+  int posr[2], lbr[2];
   float lser[2], Dr[2];
   bool rv[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int ri = mrow + g + 8 * u;
     rv[u] = ri < nr;
-    posr[u] = p.q_start + (r0 + (rv[u] ? ri : 0)) / H;
+    posr[u] = p.q_start + div_h(p, r0 + (rv[u] ? ri : 0));
+    lbr[u] = posr[u] / p.b - p.l + 1;
     lser[u] = lse_s[ri];
     Dr[u] = D_s[ri];
   }
@@ -274,6 +281,9 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_mma_kernel(MP p) {
         dp[nt][e] = d4[nt][e] + d4[nt + 2][e];
       }
     const int j0 = tile_j0(it), rlo = it < nt0 ? lo[0] : lo[1], rhi = it < nt0 ? hi[0] : hi[1];
+    // the tile lies in one b-block (b % 32 == 0; range starts are block-aligned): allowed() once per tile
+    const int kbt = j0 / p.b;
+    const bool tsink = !p.sparse || kbt < p.s;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
@@ -282,7 +292,8 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_mma_kernel(MP p) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int j = j0 + ncol + 8 * nt + 2 * t4 + e;
-          const bool ok = rv[u] && j >= rlo && j < rhi && allowed(p, posr[u], j);
+          const bool ok = rv[u] && j >= rlo && j < rhi && j < p.n_kv && (!p.causal || j <= posr[u]) &&
+                          (tsink || kbt >= lbr[u]);
           const float pv = ok ? ex2f(fmaf(s[nt][2 * u + e], p.sl2, -lser[u])) : 0.f;
           ds2[e] = pv * (dp[nt][2 * u + e] - Dr[u]);
         }
@@ -348,6 +359,8 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_mma_kernel(MP p) {
   }
   float* lse_s = reinterpret_cast<float*>(smem + kKOffL);
   float* D_s = reinterpret_cast<float*>(smem + kKOffD);
+  int* pos_s = reinterpret_cast<int*>(smem + kKOffPos);
+  int* lb_s = reinterpret_cast<int*>(smem + kKOffLb);
   for (int i = tid; i < kKKeys * (kDQK / 8); i += 256) {
     const int kj = i / (kDQK / 8), c = i - kj * (kDQK / 8);
     const int j = j0 + kj;
@@ -384,30 +397,38 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_mma_kernel(MP p) {
     for (int i = tid; i < kKRows * (kDQK / 8); i += 256) {
       const int ri = i / (kDQK / 8), c = i - ri * (kDQK / 8);
       const bool v = rb + ri < R1;
-      const int r = v ? rb + ri : 0, t = r / H, h = r - t * H;
+      const int r = v ? rb + ri : 0, t = div_h(p, r), h = r - t * H;
       cp16(sb + kKOffQ + (bb * kKRows + ri) * kQRow + 16 * c,
            p.q + bi * p.q_sb + (int64_t)t * p.q_st + (int64_t)h * p.q_sh + 8 * c, v);
     }
     for (int i = tid; i < kKRows * (kDV / 8); i += 256) {
       const int ri = i / (kDV / 8), c = i - ri * (kDV / 8);
       const bool v = rb + ri < R1;
-      const int r = v ? rb + ri : 0, t = r / H, h = r - t * H;
+      const int r = v ? rb + ri : 0, t = div_h(p, r), h = r - t * H;
       cp16(sb + kKOffDO + (bb * kKRows + ri) * kORow + 16 * c,
            p.dout + bi * p.o_sb + (int64_t)t * p.o_st + (int64_t)h * p.o_sh + 8 * c, v);
     }
     if (tid < kKRows) {
       const bool v = rb + tid < R1;
-      const int r = v ? rb + tid : 0, t = r / H, h = r - t * H;
+      const int r = v ? rb + tid : 0, t = div_h(p, r), h = r - t * H, pos = p.q_start + t;
       lse_s[bb * kKRows + tid] = v ? p.lse[((int64_t)bi * H + h) * p.n_q + t] * kLog2e : 0.f;
       D_s[bb * kKRows + tid] = v ? p.D[(int64_t)bi * rows + r] : 0.f;
+      pos_s[bb * kKRows + tid] = v ? pos : -1;  // an invalid row attends nothing (j <= -1 fails; masked below)
+      lb_s[bb * kKRows + tid] = pos / p.b - p.l + 1;
     }
     cp_commit();
   };
   const int km = 16 * (warp & 1), rn = 8 * (warp >> 1), qd = warp >> 1;
   // phase-1 C fragment: keys km + g (+8), rows rn + 2 t4 (+1)
+  // the keys' side of the selection rule, once: key j = jr[u] of block kb (the tile lies in one b-block)
   int jr[2];
+  bool jok[2];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) jr[u] = j0 + km + g + 8 * u;
+  for (int u = 0; u < 2; ++u) {
+    jr[u] = j0 + km + g + 8 * u;
+    jok[u] = jr[u] < p.n_kv;
+  }
+  const bool jsink = !p.sparse || kb < p.s;
   float acc[34][4];
 #pragma unroll
   for (int n = 0; n < 34; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
@@ -476,7 +497,9 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_mma_kernel(MP p) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int ri = rn + 2 * t4 + e, r = rb + ri;
-        const bool ok = r < R1 && allowed(p, p.q_start + r / H, jr[u]);
+        // allowed(): causal j <= pos, then sink or inside the row's local window (invalid rows: pos = -1)
+        const int pos = pos_s[bb * kKRows + ri];
+        const bool ok = r < R1 && jok[u] && (!p.causal || jr[u] <= pos) && (jsink || kb >= lb_s[bb * kKRows + ri]);
         pv[e] = ok ? ex2f(fmaf(st[2 * u + e], p.sl2, -lse_s[bb * kKRows + ri])) : 0.f;
         dsv[e] = pv[e] * (dpt[2 * u + e] - D_s[bb * kKRows + ri]);
       }
@@ -636,6 +659,7 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
   p.b = a.b;
   p.nsplit = sink_splits(a);
   p.n_sink = sink_tiles(a);
+  fastdiv_init((uint32_t)a.heads, p.h_m, p.h_p);
   const bool use_part = a.sparse && p.nsplit > 1;
   if (use_part && !part) return cudaErrorInvalidValue;
   const int64_t rows = (int64_t)a.n_q * a.heads;
