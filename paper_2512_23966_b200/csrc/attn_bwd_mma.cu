@@ -177,11 +177,13 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_mma_kernel(MP p) {
   auto tile_j0 = [&](int it) { return it < nt0 ? lo[0] + it * kRKeys : lo[1] + (it - nt0) * kRKeys; };
   auto issue_k = [&](int it, int buf) {
     const int j0 = tile_j0(it);
-    for (int i = tid; i < kRKeys * (kDQK / 8); i += 256) {
-      const int kj = i / (kDQK / 8), c = i - kj * (kDQK / 8);
-      const int j = j0 + kj;
+    {  // 8 threads per key row, 9 chunks each
+      const int kj = tid >> 3, c0 = tid & 7, j = j0 + kj;
       const bool v = j < p.n_kv;
-      cp16(sb + kROffK + (buf * kRKeys + kj) * kQRow + 16 * c, p.k + bi * p.k_sb + (int64_t)(v ? j : 0) * p.k_st + 8 * c, v);
+      const uint16_t* kg = p.k + bi * p.k_sb + (int64_t)(v ? j : 0) * p.k_st + 8 * c0;
+      const uint32_t ks = sb + kROffK + (buf * kRKeys + kj) * kQRow + 16 * c0;
+#pragma unroll
+      for (int u = 0; u < kDQK / 64; ++u) cp16(ks + 128 * u, kg + 64 * u, v);
     }
     cp_commit();
   };
@@ -394,19 +396,18 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_mma_kernel(MP p) {
   };
   const int rows = p.n_q * H;
   auto issue = [&](int rb, int R1, int bb) {
-    for (int i = tid; i < kKRows * (kDQK / 8); i += 256) {
-      const int ri = i / (kDQK / 8), c = i - ri * (kDQK / 8);
+    {  // 8 threads per row: row ri = tid / 8, 16-B chunks c = tid % 8 + 8 x (9 of q, 8 of dO)
+      const int ri = tid >> 3, c0 = tid & 7;
       const bool v = rb + ri < R1;
       const int r = v ? rb + ri : 0, t = div_h(p, r), h = r - t * H;
-      cp16(sb + kKOffQ + (bb * kKRows + ri) * kQRow + 16 * c,
-           p.q + bi * p.q_sb + (int64_t)t * p.q_st + (int64_t)h * p.q_sh + 8 * c, v);
-    }
-    for (int i = tid; i < kKRows * (kDV / 8); i += 256) {
-      const int ri = i / (kDV / 8), c = i - ri * (kDV / 8);
-      const bool v = rb + ri < R1;
-      const int r = v ? rb + ri : 0, t = div_h(p, r), h = r - t * H;
-      cp16(sb + kKOffDO + (bb * kKRows + ri) * kORow + 16 * c,
-           p.dout + bi * p.o_sb + (int64_t)t * p.o_st + (int64_t)h * p.o_sh + 8 * c, v);
+      const uint16_t* qg = p.q + bi * p.q_sb + (int64_t)t * p.q_st + (int64_t)h * p.q_sh + 8 * c0;
+      const uint16_t* og = p.dout + bi * p.o_sb + (int64_t)t * p.o_st + (int64_t)h * p.o_sh + 8 * c0;
+      const uint32_t qs = sb + kKOffQ + (bb * kKRows + ri) * kQRow + 16 * c0;
+      const uint32_t os = sb + kKOffDO + (bb * kKRows + ri) * kORow + 16 * c0;
+#pragma unroll
+      for (int u = 0; u < kDQK / 64; ++u) cp16(qs + 128 * u, qg + 64 * u, v);
+#pragma unroll
+      for (int u = 0; u < kDV / 64; ++u) cp16(os + 128 * u, og + 64 * u, v);
     }
     if (tid < kKRows) {
       const bool v = rb + tid < R1;
