@@ -51,7 +51,9 @@ constexpr int kKOffL = kKOffDS + kKKeys * kTRow;
 constexpr int kKOffD = kKOffL + 2 * kKRows * 4;
 constexpr int kKOffPos = kKOffD + 2 * kKRows * 4;  // int [2][32]: the row's position
 constexpr int kKOffLb = kKOffPos + 2 * kKRows * 4;  // int [2][32]: its first local block pos / b - l + 1
-constexpr int kKSmem = kKOffLb + 2 * kKRows * 4;
+constexpr int kPartRow = 40;                         // fp32 per partial row (32 + pad: float2 stores conflict-free)
+constexpr int kKOffPart = kKOffLb + 2 * kKRows * 4;  // fp32 [2 (S, dP)][4 k quarters][32 keys][kPartRow]
+constexpr int kKSmem = kKOffPart + 2 * 4 * kKKeys * kPartRow * 4;
 static_assert(kRSmem <= 227 * 1024 && kKSmem <= 227 * 1024, "shared memory");
 
 struct MP {
@@ -419,23 +421,22 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_mma_kernel(MP p) {
     }
     cp_commit();
   };
-  const int km = 16 * (warp & 1), rn = 8 * (warp >> 1), qd = warp >> 1;
-  // phase-1 C fragment: keys km + g (+8), rows rn + 2 t4 (+1)
-  // the keys' side of the selection rule, once: key j = jr[u] of block kb (the tile lies in one b-block)
-  int jr[2];
-  bool jok[2];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    jr[u] = j0 + km + g + 8 * u;
-    jok[u] = jr[u] < p.n_kv;
-  }
-  const bool jsink = !p.sparse || kb < p.s;
+  // phase 1: warp (key half kh, k quarter kq) keeps its A fragments K[16 keys x 144 dims] in registers for the
+  // CTA's lifetime (V = K[:, :512] reuses them) and computes partial S^T, dP^T over all 32 rows of a tile
+  // (0.5 ldmatrix per MMA); the four quarters meet in shared memory. Phase 2: keys km, dims quarter qd.
+  const int kh = warp & 1, kq = warp >> 1, km = 16 * kh, qd = kq;
+  const int ndp = 32 - 9 * kq < 9 ? 32 - 9 * kq : 9;  // dP^T k steps of this quarter (dims < 512)
+  // elementwise: thread -> key kk, rows 4 r4 .. + 3
+  const int kk = tid >> 3, r4 = 4 * (tid & 7), jk = j0 + kk;
+  const bool jokk = jk < p.n_kv, jsink = !p.sparse || kb < p.s;
+  float* part = reinterpret_cast<float*>(smem + kKOffPart);
   float acc[34][4];
 #pragma unroll
   for (int n = 0; n < 34; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
-  const uint32_t aK = sb + kKOffK + (km + (lane & 15)) * kQRow + (lane >> 4) * 16;
-  const uint32_t bQ = (rn + (lane & 7)) * kQRow + (lane >> 3) * 16;
-  const uint32_t bO = (rn + (lane & 7)) * kORow + (lane >> 3) * 16;
+  const uint32_t aK = sb + kKOffK + (km + (lane & 15)) * kQRow + (lane >> 4) * 16 + 32 * 9 * kq;
+  // B of two 8-row n tiles x one k step (rows 16 np + .., k = 16 ks + ..)
+  const uint32_t bQ = ((lane & 7) + ((lane >> 4) << 3)) * kQRow + ((lane >> 3) & 1) * 16 + 32 * 9 * kq;
+  const uint32_t bO = ((lane & 7) + ((lane >> 4) << 3)) * kORow + ((lane >> 3) & 1) * 16 + 32 * 9 * kq;
   const uint32_t aP = sb + kKOffP + (km + (lane & 15)) * kTRow + (lane >> 4) * 16;
   const uint32_t aD = sb + kKOffDS + (km + (lane & 15)) * kTRow + (lane >> 4) * 16;
   const int trow = (lane & 7) + ((lane >> 3) & 1) * 8, tcol = (lane >> 4) * 8;  // ldmatrix.trans lane address
@@ -445,7 +446,14 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_mma_kernel(MP p) {
   if (csig < L) {
     issue(crb, cre, 0);
     advance(nsig, nrb, nre);
+    cp_wait<1>();  // the K tile (committed first)
+  } else {
+    cp_wait<0>();
   }
+  __syncthreads();
+  uint32_t kfr[9][4];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) ldsm4(aK + 32 * i, kfr[i]);
   for (int bb = 0; csig < L; bb ^= 1) {
     if (nsig < L) {
       issue(nrb, nre, bb ^ 1);
@@ -455,58 +463,71 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_mma_kernel(MP p) {
     }
     __syncthreads();
     const uint32_t qbase = sb + kKOffQ + bb * kKRows * kQRow, obase = sb + kKOffDO + bb * kKRows * kORow;
-    // four independent accumulator chains per product (the k steps mod 4), summed afterwards
-    float st4[4][4] = {}, dp4[4][4] = {};
-#pragma unroll 3
-    for (int k2 = 0; k2 < kDQK / 32; k2 += 2) {
-      uint32_t a[4], b[4], b2[4];
-      ldsm4(qbase + bQ + 64 * k2, b);
-      ldsm4(qbase + bQ + 64 * k2 + 64, b2);
-      ldsm4(aK + 64 * k2, a);
-      mma(st4[0], a, b[0], b[1]);
-      ldsm4(aK + 64 * k2 + 32, a);
-      mma(st4[1], a, b[2], b[3]);
-      ldsm4(aK + 64 * k2 + 64, a);
-      mma(st4[2], a, b2[0], b2[1]);
-      ldsm4(aK + 64 * k2 + 96, a);
-      mma(st4[3], a, b2[2], b2[3]);
+    float sp[4][4] = {}, dpp[4][4] = {};
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+#pragma unroll
+      for (int np = 0; np < 2; ++np) {
+        uint32_t b[4];
+        ldsm4(qbase + bQ + 16 * np * kQRow + 32 * i, b);
+        mma(sp[2 * np], kfr[i], b[0], b[1]);
+        mma(sp[2 * np + 1], kfr[i], b[2], b[3]);
+      }
     }
-#pragma unroll 4
-    for (int k2 = 0; k2 < kDV / 32; k2 += 2) {
-      uint32_t a[4], b[4], b2[4];
-      ldsm4(obase + bO + 64 * k2, b);
-      ldsm4(obase + bO + 64 * k2 + 64, b2);
-      ldsm4(aK + 64 * k2, a);
-      mma(dp4[0], a, b[0], b[1]);
-      ldsm4(aK + 64 * k2 + 32, a);
-      mma(dp4[1], a, b[2], b[3]);
-      ldsm4(aK + 64 * k2 + 64, a);
-      mma(dp4[2], a, b2[0], b2[1]);
-      ldsm4(aK + 64 * k2 + 96, a);
-      mma(dp4[3], a, b2[2], b2[3]);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      if (i < ndp) {
+#pragma unroll
+        for (int np = 0; np < 2; ++np) {
+          uint32_t b[4];
+          ldsm4(obase + bO + 16 * np * kORow + 32 * i, b);
+          mma(dpp[2 * np], kfr[i], b[0], b[1]);
+          mma(dpp[2 * np + 1], kfr[i], b[2], b[3]);
+        }
+      }
     }
-    float st[4], dpt[4];
+    // partials: C fragment keys km + g (+8), rows 8 nt + 2 t4 (+1)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int off = (kq * kKKeys + km + g + 8 * u) * kPartRow + 8 * nt + 2 * t4;
+        *reinterpret_cast<float2*>(part + off) = make_float2(sp[nt][2 * u], sp[nt][2 * u + 1]);
+        *reinterpret_cast<float2*>(part + 4 * kKKeys * kPartRow + off) = make_float2(dpp[nt][2 * u], dpp[nt][2 * u + 1]);
+      }
+    __syncthreads();  // partials complete
+    const int rb = crb, R1 = cre;
+    float4 S4 = make_float4(0.f, 0.f, 0.f, 0.f), P4 = S4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 a = *reinterpret_cast<const float4*>(part + (q * kKKeys + kk) * kPartRow + r4);
+      const float4 d = *reinterpret_cast<const float4*>(part + 4 * kKKeys * kPartRow + (q * kKKeys + kk) * kPartRow + r4);
+      S4.x += a.x;
+      S4.y += a.y;
+      S4.z += a.z;
+      S4.w += a.w;
+      P4.x += d.x;
+      P4.y += d.y;
+      P4.z += d.z;
+      P4.w += d.w;
+    }
+    const float sv[4] = {S4.x, S4.y, S4.z, S4.w}, dv4[4] = {P4.x, P4.y, P4.z, P4.w};
+    float pv[4], dsv[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      st[e] = (st4[0][e] + st4[1][e]) + (st4[2][e] + st4[3][e]);
-      dpt[e] = (dp4[0][e] + dp4[1][e]) + (dp4[2][e] + dp4[3][e]);
+      const int ri = r4 + e, r = rb + ri;
+      // allowed(): causal j <= pos, then sink or inside the row's local window (invalid rows: pos = -1)
+      const int pos = pos_s[bb * kKRows + ri];
+      const bool ok = r < R1 && jokk && (!p.causal || jk <= pos) && (jsink || kb >= lb_s[bb * kKRows + ri]);
+      pv[e] = ok ? ex2f(fmaf(sv[e], p.sl2, -lse_s[bb * kKRows + ri])) : 0.f;
+      dsv[e] = pv[e] * (dv4[e] - D_s[bb * kKRows + ri]);
     }
-    const int rb = crb, R1 = cre;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      float pv[2], dsv[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int ri = rn + 2 * t4 + e, r = rb + ri;
-        // allowed(): causal j <= pos, then sink or inside the row's local window (invalid rows: pos = -1)
-        const int pos = pos_s[bb * kKRows + ri];
-        const bool ok = r < R1 && jok[u] && (!p.causal || jr[u] <= pos) && (jsink || kb >= lb_s[bb * kKRows + ri]);
-        pv[e] = ok ? ex2f(fmaf(st[2 * u + e], p.sl2, -lse_s[bb * kKRows + ri])) : 0.f;
-        dsv[e] = pv[e] * (dpt[2 * u + e] - D_s[bb * kKRows + ri]);
-      }
-      const uint32_t off = (km + g + 8 * u) * kTRow + (rn + 2 * t4) * 2;
-      sts32(sb + kKOffP + off, pack2(pv[0], pv[1]));
-      sts32(sb + kKOffDS + off, pack2(dsv[0], dsv[1]));
+    {
+      const uint32_t off = kk * kTRow + r4 * 2;
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(sb + kKOffP + off), "r"(pack2(pv[0], pv[1])),
+                   "r"(pack2(pv[2], pv[3])));
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(sb + kKOffDS + off), "r"(pack2(dsv[0], dsv[1])),
+                   "r"(pack2(dsv[2], dsv[3])));
     }
     __syncthreads();  // P^T, dS^T complete
     uint32_t ad0[4], ad1[4], ap0[4], ap1[4];
