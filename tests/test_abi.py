@@ -94,3 +94,16 @@ def test_seqpar_validation():
     a2 = _args(n_q=1024, n_kv=1024, q_start=1024)
     assert lib.ssa_seqpar_prefill(ctypes.byref(a2), loza.Pattern(1, 7, 128), None, 1, 2, None, 0, None) == 1
     assert lib.loza_workspace_size(loza.LOZA_WS_SEQPAR, ctypes.byref(a2), loza.Pattern(1, 7, 128), 2) > 0
+
+
+@pytest.mark.parametrize("B,n,pat,want", [
+    # D [B, n_q*H] fp32 (256-B aligned), then the tensor-core path's sink-tile partials:
+    # B x ceil(s*b/32) tiles x ceil(n_q/(l*b)) splits x 32 keys x 1088 fp32 (attn_bwd_mma.cu)
+    (2, 8192, (1, 7, 128), 2 * 8192 * 64 * 4 + 2 * 4 * 10 * 32 * 1088 * 4),
+    (1, 512, (1, 7, 128), 512 * 64 * 4),                          # one split: no partials
+    (1, 1024, (2, 1, 128), 1024 * 64 * 4 + 8 * 8 * 32 * 1088 * 4),  # two sink blocks, 8 splits
+])
+def test_backward_workspace_size(B, n, pat, want):
+    """loza_workspace_size(LOZA_WS_BACKWARD) is what attention_backward checks against (host logic only)."""
+    a = _args(batch=B, n_q=n, n_kv=n)
+    assert loza.lib().loza_workspace_size(loza.LOZA_WS_BACKWARD, ctypes.byref(a), loza.Pattern(*pat), 1) == want
