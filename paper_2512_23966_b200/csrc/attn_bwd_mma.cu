@@ -18,6 +18,8 @@
 // P and dS are rounded to bf16 as MMA operands (fp32 softmax arithmetic); bf16-path tolerance as the forward.
 // Shared-memory rows are padded by 16 B (ldmatrix conflict-free).
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "internal.h"
 
@@ -694,11 +696,21 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
     count_launch();
   }
   if (a.n_kv > 0) {
-    e = cudaFuncSetAttribute(bwd_dkdv_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKSmem);
-    if (e != cudaSuccess) return e;
-    const int64_t kt = (a.n_kv + kKKeys - 1) / kKKeys;
-    bwd_dkdv_mma_kernel<<<dim3((unsigned)(a.batch * kt), use_part ? p.nsplit : 1), 256, kKSmem, st>>>(p);
-    count_launch();
+    // key side: tcgen05 (attn_bwd_tc.cu) for the packed row layout; LOZA_BWD_KEYS=mma forces this file's kernel
+    static const bool force_mma = [] {
+      const char* ev = getenv("LOZA_BWD_KEYS");
+      return ev && strcmp(ev, "mma") == 0;
+    }();
+    if (!force_mma && backward_tc_eligible(a, dout)) {
+      e = launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, p.nsplit, p.n_sink, st);
+      if (e != cudaSuccess) return e;
+    } else {
+      e = cudaFuncSetAttribute(bwd_dkdv_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKSmem);
+      if (e != cudaSuccess) return e;
+      const int64_t kt = (a.n_kv + kKKeys - 1) / kKKeys;
+      bwd_dkdv_mma_kernel<<<dim3((unsigned)(a.batch * kt), use_part ? p.nsplit : 1), 256, kKSmem, st>>>(p);
+      count_launch();
+    }
     if (use_part) {
       const int64_t n = (int64_t)a.batch * p.n_sink * kKKeys * (kDKV / 4);
       bwd_sink_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p);

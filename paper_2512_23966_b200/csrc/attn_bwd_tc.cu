@@ -1,0 +1,427 @@
+// Attention backward, key side on the 5th-gen tensor cores: dK_j = scale sum_r dS_rj q_r and
+// dV_j = sum_r P_rj dO_r (definitions in attn_bwd_simt.cu's header) for the absorbed MLA shape (bf16, d_qk 576,
+// d_v 512, V = K[:, :512]) with tcgen05 UMMAs, fp32 accumulators in TMEM. The dQ / D side stays on the row
+// kernel of attn_bwd_mma.cu (launched first: D feeds this kernel).
+//
+// One CTA per 32 keys of one b-block (the key tile of attn_bwd_mma.cu's key kernel, same row ranges, sink
+// splits and row-block rotation), rows streamed as 128-row tiles:
+//   S   [128 rows x 32 keys] = Q K^T        (A = Q K-major, B = K K-major; M128 N32, 36 k steps)
+//   dP  [128 x 32]           = dO V^T       (32 k steps)
+//   P, dS = f(S, dP) by 4 warps (thread = row = TMEM lane), bf16 into shared memory ([rows][32 keys], SW64)
+//   dK^T [576 x 32] += Q^T dS                (A = Q^T MN-major from the same SW128 boxes; 5 M128 tiles, the
+//                                             last over dims 512..639 whose upper half TMA zero-fills)
+//   dV^T [512 x 32] += dO^T P                (4 M128 tiles)
+// TMEM: dK^T 160 + dV^T 128 + S 2x32 + dP 2x32 columns. Q / dO move as 64-dim chunk pairs [2][128 rows][64]
+// (one 4-D TMA box, 32 KB) through a 4-slot ring, twice per row tile (S/dP, then dK^T/dV^T): the tile does
+// not fit shared memory whole. Warp roles: 0 TMA, 1 UMMA issue (+ TMEM alloc), 4-7 P/dS and the epilogue.
+#include <math.h>
+
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace loza {
+
+namespace {
+
+using namespace sm100;
+
+constexpr int kKeys = 32, kRows = 128, kDqk = 576, kDv = 512, kDkv = kDqk + kDv;
+constexpr int kQPairs = 5, kOPairs = 4;        // 64-dim chunk pairs of q (the 10th chunk is OOB: zeros) and dO
+constexpr int kPairBytes = 2 * kRows * 128;    // 32 KB
+constexpr int kStages = 4;
+constexpr int kKBytes = 9 * kKeys * 128;       // 36 KB: [9 chunks][32 keys][64]
+constexpr int kPBytes = kRows * 64;            // [128 rows][32 keys] bf16, SWIZZLE_64B
+constexpr int kOffRing = 0;
+constexpr int kOffK = kOffRing + kStages * kPairBytes;
+constexpr int kOffP = kOffK + kKBytes;         // 2 buffers
+constexpr int kOffDS = kOffP + 2 * kPBytes;    // 2 buffers
+constexpr int kOffBar = kOffDS + 2 * kPBytes;
+constexpr int kBarFull = 0, kBarEmpty = kStages, kBarK = 2 * kStages, kBarSFull = kBarK + 1,
+              kBarSFree = kBarSFull + 2, kBarPReady = kBarSFree + 2, kBarPFree = kBarPReady + 2,
+              kBarAcc = kBarPFree + 2, kNumBars = kBarAcc + 1;
+constexpr int kOffTmemPtr = kOffBar + 8 * kNumBars;
+constexpr int kSmem = kOffTmemPtr + 16 + 1024;  // + alignment slack (SW128 operands: 1024-B aligned)
+constexpr uint32_t kTmemDK = 0, kTmemDV = 160, kTmemS = 288, kTmemDP = 352, kTmemCols = 512;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct TcBwdParams {
+  CUtensorMap q_map;  // {64, n_q*H rows, 9 chunks, B}, box {64, 128, 2, 1}
+  CUtensorMap o_map;  // dO: {64, n_q*H, 8, B}, box {64, 128, 2, 1}
+  CUtensorMap k_map;  // {64, n_kv, 9, B}, box {64, 32, 9, 1}
+  const float* lse;
+  const float* D;
+  float* dk;
+  float* dv;
+  float* part;
+  int32_t batch, n_q, heads, n_kv, q_start;
+  float scale, sl2;
+  int32_t sparse, causal, s, l, b;
+  int32_t nsplit, n_sink;
+  uint32_t h_m, h_p;
+};
+
+__device__ __forceinline__ int div_h(const TcBwdParams& p, int n) {
+  return (int)(((uint64_t)(uint32_t)n * p.h_m) >> p.h_p);
+}
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+  return d;
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+
+// The CTA's row tiles (all roles walk the same sequence): segments as in attn_bwd_mma.cu's key kernel.
+struct RowIter {
+  int L, m0, m1, p0, p1, R0, R1, qs, H, b;
+  int sig, rb, re;
+  __device__ void next_seg() {
+    while (++sig < L) {
+      if (L == 1) {
+        rb = R0;
+        re = R1;
+      } else {
+        const int m = m0 + ((sig - m0) % L + L) % L;
+        if (m > m1) continue;
+        const int a = m * b > p0 ? m * b : p0, e = (m + 1) * b < p1 ? (m + 1) * b : p1;
+        rb = (a - qs) * H;
+        re = (e - qs) * H;
+      }
+      if (rb < re) return;
+    }
+  }
+  __device__ void start() {
+    sig = -1;
+    rb = re = 0;
+    next_seg();
+  }
+  __device__ bool valid() const { return sig < L; }
+  __device__ void advance() {
+    rb += kRows;
+    if (rb >= re) next_seg();
+  }
+};
+
+__global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_constant__ TcBwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sbase - sraw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = p.heads;
+  const int ktiles = (p.n_kv + kKeys - 1) / kKeys;
+  const int bi = blockIdx.x / ktiles, tile = blockIdx.x - bi * ktiles, j0 = tile * kKeys;
+  // rows attending keys [j0, j0 + 32): positions [p0, p1) (as in attn_bwd_mma.cu)
+  int p0 = p.causal ? j0 : 0, p1 = p.q_start + p.n_q;
+  const int kb = j0 / p.b;
+  if (p.sparse && kb >= p.s) {
+    const int pe = (kb + p.l) * p.b;
+    if (pe < p1) p1 = pe;
+  }
+  if (p0 < p.q_start) p0 = p.q_start;
+  int R0 = 0, R1 = 0;
+  if (p1 > p0) {
+    R0 = (p0 - p.q_start) * H;
+    R1 = (p1 - p.q_start) * H;
+  }
+  const bool split = p.sparse && kb < p.s && p.nsplit > 1;
+  if (split) {
+    const int chunk = ((R1 - R0 + p.nsplit - 1) / p.nsplit + kRows - 1) / kRows * kRows;
+    const int a = R0 + (int)blockIdx.y * chunk, e = a + chunk;
+    R0 = a < R1 ? a : R1;
+    R1 = e < R1 ? e : R1;
+  } else if (blockIdx.y > 0) {
+    return;
+  }
+  RowIter it;
+  it.L = p.sparse && !split && kb >= p.s ? p.l : 1;
+  it.m0 = p0 / p.b;
+  it.m1 = (p1 - 1) / p.b;
+  it.p0 = p0;
+  it.p1 = p1;
+  it.R0 = R0;
+  it.R1 = R1;
+  it.qs = p.q_start;
+  it.H = H;
+  it.b = p.b;
+  it.start();
+  const bool any = it.valid();
+
+  auto bar = [&](int i) { return sbase + kOffBar + 8 * i; };
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kOffTmemPtr);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(bar(kBarFull + i), 1);
+      mbar_init(bar(kBarEmpty + i), 1);
+    }
+    mbar_init(bar(kBarK), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(kBarSFull + i), 1);
+      mbar_init(bar(kBarSFree + i), 4);
+      mbar_init(bar(kBarPReady + i), 4);
+      mbar_init(bar(kBarPFree + i), 1);
+    }
+    mbar_init(bar(kBarAcc), 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.q_map);
+    prefetch_tmap(&p.o_map);
+    prefetch_tmap(&p.k_map);
+  }
+  if (warp == 1) tmem_alloc<1>(smem_u32(tmem_ptr), kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0 && any) {
+      const uint64_t pol_k = policy_evict_last(), pol = policy_evict_normal();
+      mbar_arrive_expect_tx(bar(kBarK), kKBytes);
+      tma_load_4d(sbase + kOffK, &p.k_map, 0, j0, 0, bi, bar(kBarK), pol_k);
+      uint32_t slot = 0, ph = 0;
+      auto load_pair = [&](const CUtensorMap* m, int pair, int rb) {
+        mbar_wait(bar(kBarEmpty + slot), ph ^ 1);
+        mbar_arrive_expect_tx(bar(kBarFull + slot), kPairBytes);
+        tma_load_4d(sbase + kOffRing + slot * kPairBytes, m, 0, rb, 2 * pair, bi, bar(kBarFull + slot), pol);
+        if (++slot == kStages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      };
+      for (; it.valid(); it.advance()) {
+        for (int rep = 0; rep < 2; ++rep) {  // S / dP, then dK^T / dV^T
+          for (int q = 0; q < kQPairs; ++q) load_pair(&p.q_map, q, it.rb);
+          for (int q = 0; q < kOPairs; ++q) load_pair(&p.o_map, q, it.rb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ UMMA issuer
+    if (any) {
+      constexpr uint32_t id_s = idesc_bf16_f32(kRows, kKeys, false, false);
+      constexpr uint32_t id_t = idesc_bf16_f32(128, kKeys, true, true);
+      mbar_wait(bar(kBarK), 0);
+      tc_fence_after();
+      uint32_t slot = 0, ph = 0;
+      auto take = [&]() {
+        mbar_wait(bar(kBarFull + slot), ph);
+        tc_fence_after();
+      };
+      auto release = [&]() {
+        if (elect_one()) umma_commit_1sm(bar(kBarEmpty + slot));
+        __syncwarp();
+        if (++slot == kStages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      };
+      for (int tc = 0; it.valid(); it.advance(), ++tc) {
+        const int buf = tc & 1, use = tc >> 1;
+        mbar_wait(bar(kBarSFree + buf), (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tS = tmem + kTmemS + 32 * buf, tP = tmem + kTmemDP + 32 * buf;
+        for (int q = 0; q < kQPairs; ++q) {  // S = Q K^T
+          take();
+          if (elect_one()) {
+            const int nk = q < kQPairs - 1 ? 8 : 4;
+            for (int k = 0; k < nk; ++k) {
+              const uint32_t ch = 2 * q + (k >> 2), kk = k & 3;
+              umma_bf16_1sm(tS, sdesc_sw128(sbase + kOffRing + slot * kPairBytes + (k >> 2) * 16384 + 32 * kk, 16, 1024),
+                            sdesc_sw128(sbase + kOffK + ch * 4096 + 32 * kk, 16, 1024), id_s, (q | k) != 0);
+            }
+          }
+          release();
+        }
+        for (int q = 0; q < kOPairs; ++q) {  // dP = dO V^T (V = K[:, :512])
+          take();
+          if (elect_one()) {
+            for (int k = 0; k < 8; ++k) {
+              const uint32_t ch = 2 * q + (k >> 2), kk = k & 3;
+              umma_bf16_1sm(tP, sdesc_sw128(sbase + kOffRing + slot * kPairBytes + (k >> 2) * 16384 + 32 * kk, 16, 1024),
+                            sdesc_sw128(sbase + kOffK + ch * 4096 + 32 * kk, 16, 1024), id_s, (q | k) != 0);
+            }
+          }
+          release();
+        }
+        if (elect_one()) umma_commit_1sm(bar(kBarSFull + buf));
+        __syncwarp();
+        mbar_wait(bar(kBarPReady + buf), use & 1);
+        tc_fence_after();
+        const uint32_t dsb = sbase + kOffDS + buf * kPBytes, pb = sbase + kOffP + buf * kPBytes;
+        for (int q = 0; q < kQPairs; ++q) {  // dK^T[dims 128 q ..] += Q^T dS
+          take();
+          if (elect_one()) {
+            for (int kr = 0; kr < 8; ++kr)
+              umma_bf16_1sm(tmem + kTmemDK + 32 * q,
+                            sdesc_sw128(sbase + kOffRing + slot * kPairBytes + 2048 * kr, 16384, 1024),
+                            sdesc_sw64(dsb + 1024 * kr, 16, 512), id_t, (tc | kr) != 0);
+          }
+          release();
+        }
+        for (int q = 0; q < kOPairs; ++q) {  // dV^T[dims 128 q ..] += dO^T P
+          take();
+          if (elect_one()) {
+            for (int kr = 0; kr < 8; ++kr)
+              umma_bf16_1sm(tmem + kTmemDV + 32 * q,
+                            sdesc_sw128(sbase + kOffRing + slot * kPairBytes + 2048 * kr, 16384, 1024),
+                            sdesc_sw64(pb + 1024 * kr, 16, 512), id_t, (tc | kr) != 0);
+          }
+          release();
+        }
+        if (elect_one()) umma_commit_1sm(bar(kBarPFree + buf));
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit_1sm(bar(kBarAcc));
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ P / dS (thread = row = TMEM lane)
+    const int q = warp - 4, row = 32 * q + lane;
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+    const int rows = p.n_q * H;
+    const bool jsink = !p.sparse || kb < p.s;
+    for (int tc = 0; it.valid(); it.advance(), ++tc) {
+      const int buf = tc & 1, use = tc >> 1;
+      const int r = it.rb + row;
+      const bool rv = r < it.re;
+      const int rr = rv ? r : 0, t = div_h(p, rr), h = rr - t * H, pos = p.q_start + t;
+      const float lse2 = rv ? p.lse[((int64_t)bi * H + h) * p.n_q + t] * kLog2e : 0.f;
+      const float Dr = rv ? p.D[(int64_t)bi * rows + rr] : 0.f;
+      const bool win = jsink || kb >= pos / p.b - p.l + 1;
+      mbar_wait(bar(kBarSFull + buf), use & 1);
+      tc_fence_after();
+      uint32_t sv[32], dv[32];
+      tmem_ld32(tl + kTmemS + 32 * buf, sv);
+      tmem_ld32(tl + kTmemDP + 32 * buf, dv);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(bar(kBarSFree + buf));
+      uint32_t pk[16], dk2[16];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        float pv[2], ds[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = j0 + c + e;
+          const bool ok = rv && win && j < p.n_kv && (!p.causal || j <= pos);
+          pv[e] = ok ? ex2(fmaf(__uint_as_float(sv[c + e]), p.sl2, -lse2)) : 0.f;
+          ds[e] = pv[e] * (__uint_as_float(dv[c + e]) - Dr);
+        }
+        pk[c >> 1] = pack_bf16x2(pv[0], pv[1]);
+        dk2[c >> 1] = pack_bf16x2(ds[0], ds[1]);
+      }
+      mbar_wait(bar(kBarPFree + buf), (use & 1) ^ 1);
+      // row of 64 B = 4 x 16-B units, SWIZZLE_64B: unit u at (u ^ (row >> 1) & 3)
+      const uint32_t pr = sbase + kOffP + buf * kPBytes + row * 64, dr = sbase + kOffDS + buf * kPBytes + row * 64;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t o = (uint32_t)((u ^ ((row >> 1) & 3)) << 4);
+        st_shared_v4(pr + o, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        st_shared_v4(dr + o, dk2[4 * u], dk2[4 * u + 1], dk2[4 * u + 2], dk2[4 * u + 3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(bar(kBarPReady + buf));
+    }
+    // ------------------------------------------------------------------ epilogue: TMEM lane = dim, column = key
+    if (any) {
+      mbar_wait(bar(kBarAcc), 0);
+      tc_fence_after();
+    }
+    for (int m = 0; m < kQPairs + kOPairs; ++m) {
+      const bool isk = m < kQPairs;
+      const int dim = 128 * (isk ? m : m - kQPairs) + 32 * q + lane;
+      if (isk && 128 * m + 32 * q >= kDqk) continue;  // warp-uniform: dims 576.. of the last dK^T tile
+      uint32_t v[32];
+      if (any) {
+        tmem_ld32(tl + (isk ? kTmemDK + 32 * m : kTmemDV + 32 * (m - kQPairs)), v);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = 0u;
+      }
+      const float sc = isk ? p.scale : 1.f;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const int j = j0 + c;
+        if (j >= p.n_kv) continue;
+        const float x = __uint_as_float(v[c]) * sc;
+        if (split)
+          p.part[((((int64_t)bi * p.n_sink + tile) * p.nsplit + blockIdx.y) * kKeys + c) * kDkv + (isk ? 0 : kDqk) + dim] = x;
+        else if (isk)
+          p.dk[((int64_t)bi * p.n_kv + j) * kDqk + dim] = x;
+        else
+          p.dv[((int64_t)bi * p.n_kv + j) * kDv + dim] = x;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<1>(tmem, kTmemCols);
+  }
+}
+
+}  // namespace
+
+// Packed row layout (rows = tokens x heads at a uniform stride) for the 2-D row view of q and dO.
+bool backward_tc_eligible(const AttnProblem& a, const void* dout) {
+  (void)dout;
+  return a.q_st == (int64_t)a.heads * a.q_sh && a.o_st == (int64_t)a.heads * a.o_sh && a.q_sh >= 576 &&
+         a.o_sh >= 512;
+}
+
+cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
+                               float* part, int nsplit, int n_sink, cudaStream_t st) {
+  TcBwdParams p;
+  const auto& kv = a.kv.seg[0];
+  const uint64_t rows = (uint64_t)a.n_q * a.heads;
+  if (!encode_4d_chunks(&p.q_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 2) ||
+      !encode_4d_chunks(&p.o_map, dout, kDv, rows, a.batch, a.o_sh, a.o_sb, kRows, 2) ||
+      !encode_4d_chunks(&p.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, kKeys, 9))
+    return cudaErrorInvalidValue;
+  p.lse = a.lse;
+  p.D = D;
+  p.dk = dk;
+  p.dv = dv;
+  p.part = part;
+  p.batch = a.batch;
+  p.n_q = a.n_q;
+  p.heads = a.heads;
+  p.n_kv = (int32_t)a.n_kv;
+  p.q_start = (int32_t)a.q_start;
+  p.scale = a.scale;
+  p.sl2 = a.scale * kLog2e;
+  p.sparse = a.sparse;
+  p.causal = a.causal;
+  p.s = a.s;
+  p.l = a.l;
+  p.b = a.b;
+  p.nsplit = nsplit;
+  p.n_sink = n_sink;
+  {
+    uint32_t l = 0;
+    while ((1ull << l) < (uint64_t)a.heads) ++l;
+    p.h_p = 31 + l;
+    p.h_m = (uint32_t)(((1ull << p.h_p) + a.heads - 1) / a.heads);
+  }
+  cudaError_t e = cudaFuncSetAttribute(bwd_dkdv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  if (e != cudaSuccess) return e;
+  const int64_t kt = (a.n_kv + kKeys - 1) / kKeys;
+  const bool use_part = a.sparse && nsplit > 1;
+  bwd_dkdv_tc_kernel<<<dim3((unsigned)(a.batch * kt), use_part ? nsplit : 1), 256, kSmem, st>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace loza

@@ -141,7 +141,8 @@ def test_backward_tiled_fp32_h8(sparse, causal, q0):
     (False, True, 0, 8, 100, None, 1, True),            # ragged rows and keys, one partial key tile set
 ])
 def test_backward_mla_mma(sparse, causal, q0, H, n, pat, B, ofwd):
-    """The tensor-core backward (attn_bwd_mma.cu: bf16, 576/512, V = KV[:, :512]) against the fp64 oracle
+    """The tensor-core backward (attn_bwd_mma.cu row kernel + attn_bwd_tc.cu tcgen05 key kernel: bf16, 576/512,
+    V = KV[:, :512]) against the fp64 oracle
     backward, every row and key, bf16 tolerance (2e-2 normwise); deterministic across calls. ofwd: O and LSE
     from the oracle forward (rounded to bf16 / fp32), for row counts the bf16 forward does not take."""
     qs = Spec(seed=45, tensor_id=TID_Q, batch=B, n=n, heads=H, d=576)
@@ -191,4 +192,18 @@ def test_backward_mla_simt_forced():
                         os.path.join(root, "tests", "test_gpu_backward.py") + "::test_backward_mla_bf16_ssa"],
                        cwd=root, env=dict(os.environ, LOZA_BWD_KERNEL="simt"), capture_output=True, text=True,
                        timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_backward_mma_keys_forced():
+    """LOZA_BWD_KEYS=mma: the warp-level-MMA key kernel (attn_bwd_mma.cu) instead of the tcgen05 one
+    (attn_bwd_tc.cu, the default for packed layouts) through the MLA parity cases."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider", "-k", "mla",
+                        os.path.join(root, "tests", "test_gpu_backward.py")],
+                       cwd=root, env=dict(os.environ, LOZA_BWD_KEYS="mma"), capture_output=True, text=True,
+                       timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
