@@ -648,7 +648,7 @@ bool backward_mma_eligible(const AttnProblem& a, const void* dout) {
 }
 
 cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, float* dq, float* dk, float* dv,
-                                     float* D, float* part, cudaStream_t st) {
+                                     float* D, float* part, uint16_t* ds, cudaStream_t st) {
   MP p;
   const auto& kv = a.kv.seg[0];
   p.q = static_cast<const uint16_t*>(a.q);
@@ -688,6 +688,29 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
   if (use_part && !part) return cudaErrorInvalidValue;
   const int64_t rows = (int64_t)a.n_q * a.heads;
   cudaError_t e;
+  // Key side: tcgen05 (attn_bwd_tc.cu) for the packed row layout (LOZA_BWD_KEYS=mma forces this file's key
+  // kernel). SSA: the tcgen05 key kernel also writes dS rows and dQ = dS K runs as a tcgen05 GEMM
+  // (LOZA_BWD_DQ=mma keeps this file's row kernel, which recomputes S and dP).
+  static const bool force_mma = [] {
+    const char* ev = getenv("LOZA_BWD_KEYS");
+    return ev && strcmp(ev, "mma") == 0;
+  }();
+  static const bool force_dq_mma = [] {
+    const char* ev = getenv("LOZA_BWD_DQ");
+    return ev && strcmp(ev, "mma") == 0;
+  }();
+  const bool tc_keys = !force_mma && backward_tc_eligible(a, dout);
+  if (tc_keys && !force_dq_mma && ds && backward_ds_eligible(a) && rows > 0 && a.n_kv > 0) {
+    if ((e = launch_bwd_D(a, dout, D, st)) != cudaSuccess) return e;
+    if ((e = launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st)) != cudaSuccess) return e;
+    if ((e = launch_bwd_dq_tc(a, ds, dq, st)) != cudaSuccess) return e;
+    if (use_part) {
+      const int64_t n = (int64_t)a.batch * p.n_sink * kKKeys * (kDKV / 4);
+      bwd_sink_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p);
+      count_launch();
+    }
+    return cudaGetLastError();
+  }
   if (rows > 0) {
     e = cudaFuncSetAttribute(bwd_dq_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRSmem);
     if (e != cudaSuccess) return e;
@@ -696,13 +719,8 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
     count_launch();
   }
   if (a.n_kv > 0) {
-    // key side: tcgen05 (attn_bwd_tc.cu) for the packed row layout; LOZA_BWD_KEYS=mma forces this file's kernel
-    static const bool force_mma = [] {
-      const char* ev = getenv("LOZA_BWD_KEYS");
-      return ev && strcmp(ev, "mma") == 0;
-    }();
-    if (!force_mma && backward_tc_eligible(a, dout)) {
-      e = launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, p.nsplit, p.n_sink, st);
+    if (tc_keys) {
+      e = launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, nullptr, p.nsplit, p.n_sink, st);
       if (e != cudaSuccess) return e;
     } else {
       e = cudaFuncSetAttribute(bwd_dkdv_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKSmem);

@@ -629,8 +629,9 @@ __global__ void __launch_bounds__(256) bwd_keys_async_kernel(BwdParams p) {
 static size_t d_bytes(const AttnProblem& a) {
   return (sizeof(float) * (size_t)a.batch * a.n_q * a.heads + 255) / 256 * 256;
 }
-// D, then (tensor-core path, SSA) the sink-tile partials of attn_bwd_mma.cu
-size_t backward_ws_bytes(const AttnProblem& a) { return d_bytes(a) + backward_mma_part_bytes(a); }
+static size_t part_bytes(const AttnProblem& a) { return (backward_mma_part_bytes(a) + 255) / 256 * 256; }
+// D, then (tensor-core path, SSA) the sink-tile partials and the dS rows (attn_bwd_mma.cu / attn_bwd_tc.cu)
+size_t backward_ws_bytes(const AttnProblem& a) { return d_bytes(a) + part_bytes(a) + backward_ds_bytes(a); }
 
 cudaError_t launch_attn_backward(const AttnProblem& a, const void* dout, float* dq, float* dk, float* dv, void* ws,
                                  cudaStream_t st) {
@@ -641,8 +642,10 @@ cudaError_t launch_attn_backward(const AttnProblem& a, const void* dout, float* 
     return e && strcmp(e, "simt") == 0;
   }();
   if (!force_simt && backward_mma_eligible(a, dout))
-    return launch_attn_backward_mma(a, dout, dq, dk, dv, reinterpret_cast<float*>(ws),
-                                    reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + d_bytes(a)), st);
+    return launch_attn_backward_mma(
+        a, dout, dq, dk, dv, reinterpret_cast<float*>(ws), reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + d_bytes(a)),
+        backward_ds_bytes(a) ? reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(ws) + d_bytes(a) + part_bytes(a)) : nullptr,
+        st);
   BwdParams p;
   p.q = a.q;
   p.k = a.kv.seg[0].k;

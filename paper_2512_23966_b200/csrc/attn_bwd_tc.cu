@@ -53,6 +53,7 @@ struct TcBwdParams {
   float* dk;
   float* dv;
   float* part;
+  uint16_t* ds;  // SSA: dS rows [B][n_q*H][(s+l)*b] bf16 (slot = sink key, then the row's local window), or NULL
   int32_t batch, n_q, heads, n_kv, q_start;
   float scale, sl2;
   int32_t sparse, causal, s, l, b;
@@ -319,6 +320,15 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
         pk[c >> 1] = pack_bf16x2(pv[0], pv[1]);
         dk2[c >> 1] = pack_bf16x2(ds[0], ds[1]);
       }
+      if (p.ds && rv) {  // this row's 32 dS values at its slots of block kb (every row here has kb in its window)
+        int lbq = pos / p.b - p.l + 1;
+        if (lbq < p.s) lbq = p.s;
+        const int W = (p.s + p.l) * p.b;
+        const int slot = kb < p.s ? j0 : p.s * p.b + (kb - lbq) * p.b + (j0 - kb * p.b);
+        uint4* dst = reinterpret_cast<uint4*>(p.ds + ((int64_t)bi * rows + rr) * W + slot);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dst[u] = make_uint4(dk2[4 * u], dk2[4 * u + 1], dk2[4 * u + 2], dk2[4 * u + 3]);
+      }
       mbar_wait(bar(kBarPFree + buf), (use & 1) ^ 1);
       // row of 64 B = 4 x 16-B units, SWIZZLE_64B: unit u at (u ^ (row >> 1) & 3)
       const uint32_t pr = sbase + kOffP + buf * kPBytes + row * 64, dr = sbase + kOffDS + buf * kPBytes + row * 64;
@@ -372,6 +382,182 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
   }
 }
 
+// ---------------------------------------------------------------------------------------------- dQ = dS K
+// SSA only: dQ[128 rows, 192-dim slice] = scale * DS[rows, slots] K[slots -> keys, slice] as a tcgen05 GEMM
+// (M128 N192 K16, A = DS K-major, B = K MN-major over 3 64-dim atoms) from the dS rows the key kernel wrote:
+// the rows of a tile share one query block (tokens of one b-block), hence one slot -> key map: slots [0, s b)
+// are the sink keys, slots s b + i the keys lbq b + i of the local window (lbq = max(s, QB - l + 1)).
+constexpr int kQdN = 192, kQdStages = 4;
+constexpr int kQdA = kRows * 128;          // [128 rows][64 slots] bf16, SW128
+constexpr int kQdB = 3 * 64 * 128;         // [3 chunks][64 keys][64 dims], SW128
+constexpr int kQdStage = kQdA + kQdB;      // 40 KB
+constexpr int kQdOffBar = kQdStages * kQdStage;
+constexpr int kQdNumBars = 2 * kQdStages + 1;
+constexpr int kQdOffTmemPtr = kQdOffBar + 8 * kQdNumBars;
+constexpr int kQdSmem = kQdOffTmemPtr + 16 + 1024;
+
+struct TcDqParams {
+  CUtensorMap ds_map;  // 3-D {W slots, rows, B}, box {64, 128, 1}
+  CUtensorMap k_map;   // 4-D {64, n_kv, 9, B}, box {64, 64, 3, 1}
+  float* dq;
+  int32_t rows, heads, n_kv, q_start, s, l, b, kv32;
+  float scale;
+  uint32_t h_m, h_p;
+};
+
+__global__ void __launch_bounds__(256, 1) bwd_dq_tc_kernel(const __grid_constant__ TcDqParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sbase - sraw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rtiles = (p.rows + kRows - 1) / kRows;
+  const int slice = blockIdx.x % 3, rest = blockIdx.x / 3, bi = rest / rtiles, r0 = (rest - bi * rtiles) * kRows;
+  const int t0 = (int)(((uint64_t)(uint32_t)r0 * p.h_m) >> p.h_p), QB = (p.q_start + t0) / p.b;
+  int lbq = QB - p.l + 1;
+  if (lbq < p.s) lbq = p.s;
+  // Slots the key kernel wrote for every row of the tile: keys below the 32-key boundary after the tile's last
+  // position (a tile's 128 / H <= 32 tokens never straddle such a boundary; keys past a row's own position
+  // inside it carry dS = 0). Beyond it a row was never visited by the key tile's CTA.
+  const int rl = r0 + kRows - 1 < p.rows ? r0 + kRows - 1 : p.rows - 1;
+  const int tl = (int)(((uint64_t)(uint32_t)rl * p.h_m) >> p.h_p);
+  const int lim = (p.q_start + tl + 1 + 31) / 32 * 32;
+  const int se = p.s * p.b < lim ? p.s * p.b : lim;
+  const int hil = (QB + 1) * p.b < lim ? (QB + 1) * p.b : lim;
+  const int nl = hil > lbq * p.b ? hil - lbq * p.b : 0;
+  const int nsc = (se + 63) / 64, nch = nsc + (nl + 63) / 64;
+  // chunk c: first slot, first key, k steps (16 slots each)
+  auto chunk = [&](int c, int& slot, int& key, int& nk) {
+    if (c < nsc) {
+      slot = key = 64 * c;
+      nk = (se - 64 * c) >= 64 ? 4 : (se - 64 * c) / 16;
+    } else {
+      const int i = 64 * (c - nsc);
+      slot = p.s * p.b + i;
+      key = lbq * p.b + i;
+      nk = (nl - i) >= 64 ? 4 : (nl - i) / 16;
+    }
+  };
+  auto bar = [&](int i) { return sbase + kQdOffBar + 8 * i; };
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kQdOffTmemPtr);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kQdStages; ++i) {
+      mbar_init(bar(i), 1);
+      mbar_init(bar(kQdStages + i), 1);
+    }
+    mbar_init(bar(2 * kQdStages), 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.ds_map);
+    prefetch_tmap(&p.k_map);
+  }
+  if (warp == 1) tmem_alloc<1>(smem_u32(tmem_ptr), 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_normal(), pol_k = policy_evict_last();
+      uint32_t slot = 0, ph = 0;
+      for (int c = 0; c < nch; ++c) {
+        int sl, key, nk;
+        chunk(c, sl, key, nk);
+        mbar_wait(bar(kQdStages + slot), ph ^ 1);
+        mbar_arrive_expect_tx(bar(slot), kQdStage);
+        const uint32_t dst = sbase + slot * kQdStage;
+        tma_load_3d(dst, &p.ds_map, sl, r0, bi, bar(slot), pol);
+        tma_load_4d(dst + kQdA, &p.k_map, 0, key, 3 * slice, bi, bar(slot), pol_k);
+        if (++slot == kQdStages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id = idesc_bf16_f32(kRows, kQdN, false, true);
+    uint32_t slot = 0, ph = 0;
+    for (int c = 0; c < nch; ++c) {
+      int sl, key, nk;
+      chunk(c, sl, key, nk);
+      mbar_wait(bar(slot), ph);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t a = sbase + slot * kQdStage;
+        for (int k = 0; k < nk; ++k)
+          umma_bf16_1sm(tmem, sdesc_sw128(a + 32 * k, 16, 1024), sdesc_sw128(a + kQdA + 2048 * k, 8192, 1024), id,
+                        (c | k) != 0);
+        umma_commit_1sm(bar(kQdStages + slot));
+      }
+      __syncwarp();
+      if (++slot == kQdStages) {
+        slot = 0;
+        ph ^= 1;
+      }
+    }
+    if (elect_one()) umma_commit_1sm(bar(2 * kQdStages));
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp - 4, row = 32 * q + lane, r = r0 + row;
+    if (nch > 0) {
+      mbar_wait(bar(2 * kQdStages), 0);
+      tc_fence_after();
+    }
+    float* out = p.dq + ((int64_t)bi * p.rows + r) * kDqk + kQdN * slice;
+    for (int g = 0; g < kQdN / 32; ++g) {
+      uint32_t v[32];
+      if (nch > 0) {
+        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 32 * g, v);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = 0u;
+      }
+      if (r < p.rows) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 4)
+          *reinterpret_cast<float4*>(out + 32 * g + c) =
+              make_float4(__uint_as_float(v[c]) * p.scale, __uint_as_float(v[c + 1]) * p.scale,
+                          __uint_as_float(v[c + 2]) * p.scale, __uint_as_float(v[c + 3]) * p.scale);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<1>(tmem, 256);
+  }
+}
+
+// D_r = dO_r . O_r (fp32), one warp per row (bf16 O and dO with o's strides, d_v 512)
+__global__ void __launch_bounds__(256) bwd_D_kernel(const uint16_t* o, const uint16_t* dout, float* D, int32_t rows,
+                                                   int32_t batch, int64_t o_sb, int64_t o_st, int64_t o_sh,
+                                                   uint32_t h_m, uint32_t h_p, int32_t H) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= (int64_t)batch * rows) return;
+  const int bi = (int)(gw / rows), r = (int)(gw - (int64_t)bi * rows);
+  const int t = (int)(((uint64_t)(uint32_t)r * h_m) >> h_p), h = r - t * H;
+  const int64_t off = bi * o_sb + (int64_t)t * o_st + (int64_t)h * o_sh;
+  float acc = 0.f;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const uint4 ov = *reinterpret_cast<const uint4*>(o + off + 8 * (lane + 32 * u));
+    const uint4 dv = *reinterpret_cast<const uint4*>(dout + off + 8 * (lane + 32 * u));
+    const uint32_t oa[4] = {ov.x, ov.y, ov.z, ov.w}, da[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      acc = fmaf(__uint_as_float(oa[e] << 16), __uint_as_float(da[e] << 16), acc);
+      acc = fmaf(__uint_as_float(oa[e] & 0xFFFF0000u), __uint_as_float(da[e] & 0xFFFF0000u), acc);
+    }
+  }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2);
+  if (lane == 0) D[gw] = acc;
+}
+
 }  // namespace
 
 // Packed row layout (rows = tokens x heads at a uniform stride) for the 2-D row view of q and dO.
@@ -382,7 +568,7 @@ bool backward_tc_eligible(const AttnProblem& a, const void* dout) {
 }
 
 cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
-                               float* part, int nsplit, int n_sink, cudaStream_t st) {
+                               float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st) {
   TcBwdParams p;
   const auto& kv = a.kv.seg[0];
   const uint64_t rows = (uint64_t)a.n_q * a.heads;
@@ -395,6 +581,7 @@ cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk
   p.dk = dk;
   p.dv = dv;
   p.part = part;
+  p.ds = ds;
   p.batch = a.batch;
   p.n_q = a.n_q;
   p.heads = a.heads;
@@ -420,6 +607,61 @@ cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk
   const int64_t kt = (a.n_kv + kKeys - 1) / kKeys;
   const bool use_part = a.sparse && nsplit > 1;
   bwd_dkdv_tc_kernel<<<dim3((unsigned)(a.batch * kt), use_part ? nsplit : 1), 256, kSmem, st>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// dS-buffer path (SSA): rows of a 128-row tile must share one query block
+bool backward_ds_eligible(const AttnProblem& a) {
+  if (!a.sparse) return false;
+  const int H = a.heads;
+  return a.causal && (H % kRows == 0 || (kRows % H == 0 && kRows / H <= 32 && a.b % (kRows / H) == 0));
+}
+size_t backward_ds_bytes(const AttnProblem& a) {
+  if (!a.sparse) return 0;
+  return (size_t)2 * a.batch * a.n_q * a.heads * ((size_t)(a.s + a.l) * a.b);
+}
+
+cudaError_t launch_bwd_D(const AttnProblem& a, const void* dout, float* D, cudaStream_t st) {
+  const int64_t rows = (int64_t)a.n_q * a.heads, warps = rows * a.batch;
+  uint32_t l = 0;
+  while ((1ull << l) < (uint64_t)a.heads) ++l;
+  const uint32_t hp = 31 + l, hm = (uint32_t)(((1ull << hp) + a.heads - 1) / a.heads);
+  bwd_D_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(static_cast<const uint16_t*>(a.o),
+                                                             static_cast<const uint16_t*>(dout), D, (int32_t)rows,
+                                                             a.batch, a.o_sb, a.o_st, a.o_sh, hm, hp, a.heads);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq, cudaStream_t st) {
+  TcDqParams p;
+  const auto& kv = a.kv.seg[0];
+  const int W = (a.s + a.l) * a.b;
+  const uint64_t rows = (uint64_t)a.n_q * a.heads;
+  if (!encode_3d(&p.ds_map, ds, (uint64_t)W, rows, a.batch, W, (int64_t)rows * W, kRows) ||
+      !encode_4d_chunks(&p.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, 64, 3))
+    return cudaErrorInvalidValue;
+  p.dq = dq;
+  p.rows = (int32_t)rows;
+  p.heads = a.heads;
+  p.n_kv = (int32_t)a.n_kv;
+  p.q_start = (int32_t)a.q_start;
+  p.s = a.s;
+  p.l = a.l;
+  p.b = a.b;
+  p.kv32 = (int32_t)((a.n_kv + 31) / 32 * 32);
+  p.scale = a.scale;
+  {
+    uint32_t l = 0;
+    while ((1ull << l) < (uint64_t)a.heads) ++l;
+    p.h_p = 31 + l;
+    p.h_m = (uint32_t)(((1ull << p.h_p) + a.heads - 1) / a.heads);
+  }
+  cudaError_t e = cudaFuncSetAttribute(bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kQdSmem);
+  if (e != cudaSuccess) return e;
+  const int64_t rt = ((int64_t)rows + kRows - 1) / kRows;
+  bwd_dq_tc_kernel<<<(unsigned)(a.batch * rt * 3), 256, kQdSmem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }

@@ -78,12 +78,17 @@ size_t backward_ws_bytes(const AttnProblem& a);
 bool backward_mma_eligible(const AttnProblem& a, const void* dout);
 size_t backward_mma_part_bytes(const AttnProblem& a);
 cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, float* dq, float* dk, float* dv,
-                                     float* D, float* part, cudaStream_t st);
+                                     float* D, float* part, uint16_t* ds, cudaStream_t st);
 // tcgen05 key side of the backward (attn_bwd_tc.cu): dK, dV (or the sink-split partials) from D; needs the
 // packed token x head row layout of q and d_o
 bool backward_tc_eligible(const AttnProblem& a, const void* dout);
 cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
-                               float* part, int nsplit, int n_sink, cudaStream_t st);
+                               float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st);
+// SSA dS-row buffer [B][n_q*H][(s+l)*b] bf16 (written by the tcgen05 key kernel) and dQ = dS K on tcgen05
+bool backward_ds_eligible(const AttnProblem& a);
+size_t backward_ds_bytes(const AttnProblem& a);
+cudaError_t launch_bwd_D(const AttnProblem& a, const void* dout, float* D, cudaStream_t st);
+cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq, cudaStream_t st);
 cudaError_t launch_attn_backward(const AttnProblem& a, const void* dout, float* dq, float* dk, float* dv, void* ws,
                                  cudaStream_t st);
 cudaError_t launch_ring_append(const void* rows, int64_t r_sb, int64_t r_st, int32_t m, const int32_t* pos0,

@@ -97,11 +97,12 @@ def test_seqpar_validation():
 
 
 @pytest.mark.parametrize("B,n,pat,want", [
-    # D [B, n_q*H] fp32 (256-B aligned), then the tensor-core path's sink-tile partials:
-    # B x ceil(s*b/32) tiles x ceil(n_q/(l*b)) splits x 32 keys x 1088 fp32 (attn_bwd_mma.cu)
-    (2, 8192, (1, 7, 128), 2 * 8192 * 64 * 4 + 2 * 4 * 10 * 32 * 1088 * 4),
-    (1, 512, (1, 7, 128), 512 * 64 * 4),                          # one split: no partials
-    (1, 1024, (2, 1, 128), 1024 * 64 * 4 + 8 * 8 * 32 * 1088 * 4),  # two sink blocks, 8 splits
+    # D [B, n_q*H] fp32 (256-B aligned), the sink-tile partials of the tensor-core key kernels
+    # (B x ceil(s*b/32) tiles x ceil(n_q/(l*b)) splits x 32 keys x 1088 fp32), then (SSA) the dS rows
+    # [B, n_q*H, (s+l)*b] bf16 the tcgen05 dQ GEMM reads (attn_bwd_mma.cu / attn_bwd_tc.cu)
+    (2, 8192, (1, 7, 128), 2 * 8192 * 64 * 4 + 2 * 4 * 10 * 32 * 1088 * 4 + 2 * 2 * 8192 * 64 * 1024),
+    (1, 512, (1, 7, 128), 512 * 64 * 4 + 2 * 512 * 64 * 1024),                        # one split: no partials
+    (1, 1024, (2, 1, 128), 1024 * 64 * 4 + 8 * 8 * 32 * 1088 * 4 + 2 * 1024 * 64 * 384),  # two sink blocks, 8 splits
 ])
 def test_backward_workspace_size(B, n, pat, want):
     """loza_workspace_size(LOZA_WS_BACKWARD) is what attention_backward checks against (host logic only)."""

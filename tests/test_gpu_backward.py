@@ -141,8 +141,8 @@ def test_backward_tiled_fp32_h8(sparse, causal, q0):
     (False, True, 0, 8, 100, None, 1, True),            # ragged rows and keys, one partial key tile set
 ])
 def test_backward_mla_mma(sparse, causal, q0, H, n, pat, B, ofwd):
-    """The tensor-core backward (attn_bwd_mma.cu row kernel + attn_bwd_tc.cu tcgen05 key kernel: bf16, 576/512,
-    V = KV[:, :512]) against the fp64 oracle
+    """The tensor-core backward (SSA: D, tcgen05 key kernel writing dS rows, tcgen05 dQ = dS K; full attention:
+    the attn_bwd_mma.cu row kernel + tcgen05 key kernel; bf16, 576/512, V = KV[:, :512]) against the fp64 oracle
     backward, every row and key, bf16 tolerance (2e-2 normwise); deterministic across calls. ofwd: O and LSE
     from the oracle forward (rounded to bf16 / fp32), for row counts the bf16 forward does not take."""
     qs = Spec(seed=45, tensor_id=TID_Q, batch=B, n=n, heads=H, d=576)
@@ -195,15 +195,16 @@ def test_backward_mla_simt_forced():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-def test_backward_mma_keys_forced():
-    """LOZA_BWD_KEYS=mma: the warp-level-MMA key kernel (attn_bwd_mma.cu) instead of the tcgen05 one
-    (attn_bwd_tc.cu, the default for packed layouts) through the MLA parity cases."""
+@pytest.mark.parametrize("env", [{"LOZA_BWD_KEYS": "mma"}, {"LOZA_BWD_DQ": "mma"}])
+def test_backward_mma_paths_forced(env):
+    """The warp-level-MMA kernels of attn_bwd_mma.cu kept reachable through the MLA parity cases:
+    LOZA_BWD_KEYS=mma (its key kernel and row kernel instead of the tcgen05 key kernel and dS GEMM) and
+    LOZA_BWD_DQ=mma (tcgen05 key kernel, dQ by the row kernel instead of the tcgen05 dS GEMM)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider", "-k", "mla",
                         os.path.join(root, "tests", "test_gpu_backward.py")],
-                       cwd=root, env=dict(os.environ, LOZA_BWD_KEYS="mma"), capture_output=True, text=True,
-                       timeout=900)
+                       cwd=root, env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
