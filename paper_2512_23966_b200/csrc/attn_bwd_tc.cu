@@ -197,11 +197,20 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
           ph ^= 1;
         }
       };
+      // the UMMA issuer's order: S/dP of tile t + 1 before dK^T/dV^T of tile t
+      auto load_tile = [&](int rb) {
+        for (int q = 0; q < kQPairs; ++q) load_pair(&p.q_map, q, rb);
+        for (int q = 0; q < kOPairs; ++q) load_pair(&p.o_map, q, rb);
+      };
+      RowIter ia = it;
+      load_tile(ia.rb);
+      ia.advance();
       for (; it.valid(); it.advance()) {
-        for (int rep = 0; rep < 2; ++rep) {  // S / dP, then dK^T / dV^T
-          for (int q = 0; q < kQPairs; ++q) load_pair(&p.q_map, q, it.rb);
-          for (int q = 0; q < kOPairs; ++q) load_pair(&p.o_map, q, it.rb);
+        if (ia.valid()) {
+          load_tile(ia.rb);
+          ia.advance();
         }
+        load_tile(it.rb);
       }
     }
   } else if (warp == 1) {
@@ -224,7 +233,9 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
           ph ^= 1;
         }
       };
-      for (int tc = 0; it.valid(); it.advance(), ++tc) {
+      // S/dP of tile t + 1 are issued before dK^T/dV^T of tile t (S/dP and P/dS double-buffered), so the
+      // tensor pipe works while the four P/dS warps process tile t
+      auto issue_sdp = [&](int tc) {
         const int buf = tc & 1, use = tc >> 1;
         mbar_wait(bar(kBarSFree + buf), (use & 1) ^ 1);
         tc_fence_after();
@@ -254,6 +265,9 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
         }
         if (elect_one()) umma_commit_1sm(bar(kBarSFull + buf));
         __syncwarp();
+      };
+      auto issue_grad = [&](int tc) {
+        const int buf = tc & 1, use = tc >> 1;
         mbar_wait(bar(kBarPReady + buf), use & 1);
         tc_fence_after();
         const uint32_t dsb = sbase + kOffDS + buf * kPBytes, pb = sbase + kOffP + buf * kPBytes;
@@ -279,6 +293,17 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
         }
         if (elect_one()) umma_commit_1sm(bar(kBarPFree + buf));
         __syncwarp();
+      };
+      RowIter ia = it;
+      issue_sdp(0);
+      ia.advance();
+      int ta = 1;
+      for (int tc = 0; it.valid(); it.advance(), ++tc) {
+        if (ia.valid()) {
+          issue_sdp(ta++);
+          ia.advance();
+        }
+        issue_grad(tc);
       }
       if (elect_one()) umma_commit_1sm(bar(kBarAcc));
       __syncwarp();
