@@ -451,10 +451,8 @@ def extra_rows(args, q, kv, o, flush, peaks):
     out["backward_ssa_8k"] = {
         "ms": bw_ms, "tflops": bw_flop / (bw_ms * 1e-3) / 1e12,
         "frac_tensor": bw_flop / (bw_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
-        # the warp-level MMA it runs on peaks at ~1024 MAC/clk/SM on B200 (tools/hmma_rate.cu: ~530 TFLOP/s)
-        "frac_mma_sync_peak": bw_flop / (bw_ms * 1e-3) / 1e12 / 530.0,
-        "kernel": "warp-level bf16 MMA (attn_bwd_mma.cu: dQ row kernel, [dK|dV] key kernel, sink tiles split "
-                  "over row ranges + fixed-order reduce); the FFMA kernels (attn_bwd_simt.cu) measured 492 ms",
+        "kernel": "tcgen05 (attn_bwd_tc.cu: D, key kernel -> dK/dV in TMEM + dS rows, dQ = dS K GEMM; sink "
+                  "tiles split over row ranges + fixed-order reduce); warp-MMA 22 ms, FFMA 492 ms before it",
         "algorithmic_flop": bw_flop}
     del of, osp, dh, oh
     # non-absorbed (MHA-form) SSA prefill: per-head K/V (192 / 128) at the headline's 32K
