@@ -3,9 +3,9 @@
 //   D_r = dO_r . O_r ;  P_rj = exp(scale q_r . k_j - LSE_r) ;  dS_rj = P_rj (dO_r . v_j - D_r)
 //   dQ_r = scale sum_j dS_rj k_j ;  dK_j = scale sum_r dS_rj q_r ;  dV_j = sum_r P_rj dO_r
 // for the absorbed MLA shape (bf16, d_qk 576, d_v 512, V = the first 512 columns of the latent row K), with
-// warp-level mma.sync m16n8k16 (bf16 operands, fp32 accumulators). The MLA head dims make the dK / dV
-// accumulators of a key tile (32 keys x 1088 fp32 = 139 KB) too large for TMEM next to the S tiles, and the
-// register file holds them when spread over 8 warps -- the warp-level MMA is the first tensor-core backward.
+// warp-level mma.sync m16n8k16 (bf16 operands, fp32 accumulators): the dK / dV accumulators of a key tile
+// (32 keys x 1088 fp32 = 139 KB) spread over 8 warps' registers. The first tensor-core backward; the default
+// is now attn_bwd_tc.cu (tcgen05, accumulators transposed in TMEM) where its layout conditions hold.
 // Deterministic, no atomics:
 //  - row kernel: 64 query rows (flattened token x head, one key set per token) per CTA; Q / dO rows resident
 //    in shared memory, 32-key K tiles double-buffered with cp.async; S, dP -> dS (bf16, shared) -> dQ += dS K
