@@ -12,7 +12,7 @@
 //                                             last over dims 512..639 whose upper half TMA zero-fills)
 //   dV^T [512 x 32] += dO^T P                (4 M128 tiles)
 // TMEM: dK^T 160 + dV^T 128 + S 2x32 + dP 2x32 columns. Q / dO move as 64-dim chunk pairs [2][128 rows][64]
-// (one 4-D TMA box, 32 KB) through a 4-slot ring, twice per row tile (S/dP, then dK^T/dV^T): the tile does
+// (one 4-D TMA box, 32 KB) through a 5-slot ring, twice per row tile (S/dP, then dK^T/dV^T): the tile does
 // not fit shared memory whole. Warp roles: 0 TMA, 1 UMMA issue (+ TMEM alloc), 4-7 P/dS and the epilogue.
 #include <math.h>
 
@@ -28,14 +28,15 @@ using namespace sm100;
 constexpr int kKeys = 32, kRows = 128, kDqk = 576, kDv = 512, kDkv = kDqk + kDv;
 constexpr int kQPairs = 5, kOPairs = 4;        // 64-dim chunk pairs of q (the 10th chunk is OOB: zeros) and dO
 constexpr int kPairBytes = 2 * kRows * 128;    // 32 KB
-constexpr int kStages = 4;
+constexpr int kStages = 5;
+constexpr int kPBufs = 1;  // P/dS buffers (one: the shared memory goes to a 5th ring slot)
 constexpr int kKBytes = 9 * kKeys * 128;       // 36 KB: [9 chunks][32 keys][64]
 constexpr int kPBytes = kRows * 64;            // [128 rows][32 keys] bf16, SWIZZLE_64B
 constexpr int kOffRing = 0;
 constexpr int kOffK = kOffRing + kStages * kPairBytes;
 constexpr int kOffP = kOffK + kKBytes;         // 2 buffers
-constexpr int kOffDS = kOffP + 2 * kPBytes;    // 2 buffers
-constexpr int kOffBar = kOffDS + 2 * kPBytes;
+constexpr int kOffDS = kOffP + kPBufs * kPBytes;
+constexpr int kOffBar = kOffDS + kPBufs * kPBytes;
 constexpr int kBarFull = 0, kBarEmpty = kStages, kBarK = 2 * kStages, kBarSFull = kBarK + 1,
               kBarSFree = kBarSFull + 2, kBarPReady = kBarSFree + 2, kBarPFree = kBarPReady + 2,
               kBarAcc = kBarPFree + 2, kNumBars = kBarAcc + 1;
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
         __syncwarp();
       };
       auto issue_grad = [&](int tc) {
-        const int buf = tc & 1, use = tc >> 1;
+        const int buf = tc % kPBufs, use = tc / kPBufs;
         mbar_wait(bar(kBarPReady + buf), use & 1);
         tc_fence_after();
         const uint32_t dsb = sbase + kOffDS + buf * kPBytes, pb = sbase + kOffP + buf * kPBytes;
@@ -354,9 +355,10 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
 #pragma unroll
         for (int u = 0; u < 4; ++u) dst[u] = make_uint4(dk2[4 * u], dk2[4 * u + 1], dk2[4 * u + 2], dk2[4 * u + 3]);
       }
-      mbar_wait(bar(kBarPFree + buf), (use & 1) ^ 1);
+      const int pbuf = tc % kPBufs, puse = tc / kPBufs;
+      mbar_wait(bar(kBarPFree + pbuf), (puse & 1) ^ 1);
       // row of 64 B = 4 x 16-B units, SWIZZLE_64B: unit u at (u ^ (row >> 1) & 3)
-      const uint32_t pr = sbase + kOffP + buf * kPBytes + row * 64, dr = sbase + kOffDS + buf * kPBytes + row * 64;
+      const uint32_t pr = sbase + kOffP + pbuf * kPBytes + row * 64, dr = sbase + kOffDS + pbuf * kPBytes + row * 64;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const uint32_t o = (uint32_t)((u ^ ((row >> 1) & 3)) << 4);
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive_local(bar(kBarPReady + buf));
+      if (lane == 0) mbar_arrive_local(bar(kBarPReady + pbuf));
     }
     // ------------------------------------------------------------------ epilogue: TMEM lane = dim, column = key
     if (any) {
