@@ -147,9 +147,12 @@ loza_status_t ssa_prefill_blend(const loza_attn_args_t* args, loza_pattern_t pat
  *   d_k [B, n_kv, d_qk]   = scale * sum_r dS_rj q_r,    P_rj  = exp(scale q_r . k_j - lse_r)
  *   d_v [B, n_kv, d_v]    = sum_r P_rj d_o_r
  * summed over every query row (all heads) that attends the key. For the absorbed MLA cache (v = the first
- * d_v columns of k) the cache gradient is d_k + [d_v, 0]. First GPU path: FFMA, fp32 accumulation,
- * deterministic (no atomics); d_qk <= 576, d_v <= 512 (else LOZA_ERR_UNSUPPORTED).
- * ws: loza_workspace_size(LOZA_WS_BACKWARD, args, pattern, 1) bytes. */
+ * d_v columns of k) the cache gradient is d_k + [d_v, 0]. Deterministic (no atomics), fp32 accumulation;
+ * d_qk <= 576, d_v <= 512 (else LOZA_ERR_UNSUPPORTED). bf16 with d_qk 576, d_v 512 and v aliasing k runs
+ * on the tensor cores (tcgen05 when q / d_o rows are packed token x head; P and dS enter the second
+ * products as bf16), everything else on FFMA.
+ * ws: loza_workspace_size(LOZA_WS_BACKWARD, args, pattern, 1) bytes: D [B, n_q*H] fp32, for SSA the sink-tile
+ * partials and the dS rows [B, n_q*H, (s+l)*b] bf16 (1 GiB at B1, 8K tokens, H64, (1,7,128)). */
 loza_status_t attention_backward(const loza_attn_args_t* args, int32_t sparse, loza_pattern_t pattern,
                                  const void* d_o, float* d_q, float* d_k, float* d_v, void* ws, size_t ws_bytes,
                                  loza_stream_t stream);
