@@ -139,6 +139,8 @@ def test_backward_tiled_fp32_h8(sparse, causal, q0):
     (False, False, 0, 8, 208, None, 1, False),          # bidirectional
     (True, True, 0, 8, 300, (1, 1, 128), 1, True),      # ragged row tile (2400 rows), 3 sink splits
     (False, True, 0, 8, 100, None, 1, True),            # ragged rows and keys, one partial key tile set
+    (True, True, 0, 24, 300, (1, 1, 128), 1, True),     # H = 24: tcgen05 keys, dQ by the warp-MMA row kernel
+    (True, True, 0, 128, 300, (1, 1, 128), 1, True),    # H = 128: one token per 128-row dQ tile
 ])
 def test_backward_mla_mma(sparse, causal, q0, H, n, pat, B, ofwd):
     """The tensor-core backward (SSA: D, tcgen05 key kernel writing dS rows, tcgen05 dQ = dS K; full attention:
