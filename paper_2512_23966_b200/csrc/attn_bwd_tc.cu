@@ -419,7 +419,7 @@ constexpr int kQdA = kRows * 128;          // [128 rows][64 slots] bf16, SW128
 constexpr int kQdB = 3 * 64 * 128;         // [3 chunks][64 keys][64 dims], SW128
 constexpr int kQdStage = kQdA + kQdB;      // 40 KB
 constexpr int kQdOffBar = kQdStages * kQdStage;
-constexpr int kQdNumBars = 2 * kQdStages + 1;
+constexpr int kQdNumBars = 2 * kQdStages + 4;
 constexpr int kQdOffTmemPtr = kQdOffBar + 8 * kQdNumBars;
 constexpr int kQdSmem = kQdOffTmemPtr + 16 + 1024;
 
@@ -427,7 +427,7 @@ struct TcDqParams {
   CUtensorMap ds_map;  // 3-D {W slots, rows, B}, box {64, 128, 1}
   CUtensorMap k_map;   // 4-D {64, n_kv, 9, B}, box {64, 64, 3, 1}
   float* dq;
-  int32_t rows, heads, n_kv, q_start, s, l, b, kv32;
+  int32_t rows, heads, n_kv, q_start, s, l, b, kv32, batch;
   float scale;
   uint32_t h_m, h_p;
 };
@@ -439,47 +439,65 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_tc_kernel(const __grid_constant
   uint8_t* smem = smem_raw + (sbase - sraw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rtiles = (p.rows + kRows - 1) / kRows;
-  const int slice = blockIdx.x % 3, rest = blockIdx.x / 3, bi = rest / rtiles, r0 = (rest - bi * rtiles) * kRows;
-  const int t0 = (int)(((uint64_t)(uint32_t)r0 * p.h_m) >> p.h_p), QB = (p.q_start + t0) / p.b;
-  int lbq = QB - p.l + 1;
-  if (lbq < p.s) lbq = p.s;
-  // Slots the key kernel wrote for every row of the tile: keys below the 32-key boundary after the tile's last
-  // position (a tile's 128 / H <= 32 tokens never straddle such a boundary; keys past a row's own position
-  // inside it carry dS = 0). Beyond it a row was never visited by the key tile's CTA.
-  const int rl = r0 + kRows - 1 < p.rows ? r0 + kRows - 1 : p.rows - 1;
-  const int tl = (int)(((uint64_t)(uint32_t)rl * p.h_m) >> p.h_p);
-  const int lim = (p.q_start + tl + 1 + 31) / 32 * 32;
-  const int se = p.s * p.b < lim ? p.s * p.b : lim;
-  const int hil = (QB + 1) * p.b < lim ? (QB + 1) * p.b : lim;
-  const int nl = hil > lbq * p.b ? hil - lbq * p.b : 0;
-  const int nsc = (se + 63) / 64, nch = nsc + (nl + 63) / 64;
-  // chunk c: first slot, first key, k steps (16 slots each)
-  auto chunk = [&](int c, int& slot, int& key, int& nk) {
-    if (c < nsc) {
+  const int ntiles = p.batch * rtiles * 3;
+  // Persistent: tiles (128 rows, 192-dim slice) strided over the grid; the dQ accumulator is double-buffered
+  // in TMEM (2 x 192 columns) so a tile's epilogue overlaps the next tile's loads and MMAs.
+  struct Tile {
+    int bi, r0, slice, lbq, se, nl, nsc, nch;
+  };
+  auto decode = [&](int t) {
+    Tile T;
+    T.slice = t % 3;
+    const int rest = t / 3;
+    T.bi = rest / rtiles;
+    T.r0 = (rest - T.bi * rtiles) * kRows;
+    const int t0 = (int)(((uint64_t)(uint32_t)T.r0 * p.h_m) >> p.h_p), QB = (p.q_start + t0) / p.b;
+    T.lbq = QB - p.l + 1 < p.s ? p.s : QB - p.l + 1;
+    // Slots the key kernel wrote for every row of the tile: keys below the 32-key boundary after the tile's
+    // last position (a tile's 128 / H <= 32 tokens never straddle such a boundary; keys past a row's own
+    // position inside it carry dS = 0). Beyond it a row was never visited by the key tile's CTA.
+    const int rl = T.r0 + kRows - 1 < p.rows ? T.r0 + kRows - 1 : p.rows - 1;
+    const int tl = (int)(((uint64_t)(uint32_t)rl * p.h_m) >> p.h_p);
+    const int lim = (p.q_start + tl + 1 + 31) / 32 * 32;
+    T.se = p.s * p.b < lim ? p.s * p.b : lim;
+    const int hil = (QB + 1) * p.b < lim ? (QB + 1) * p.b : lim;
+    T.nl = hil > T.lbq * p.b ? hil - T.lbq * p.b : 0;
+    T.nsc = (T.se + 63) / 64;
+    T.nch = T.nsc + (T.nl + 63) / 64;
+    return T;
+  };
+  // chunk c of a tile: first slot, first key, k steps (16 slots each)
+  auto chunk = [&](const Tile& T, int c, int& slot, int& key, int& nk) {
+    if (c < T.nsc) {
       slot = key = 64 * c;
-      nk = (se - 64 * c) >= 64 ? 4 : (se - 64 * c) / 16;
+      nk = (T.se - 64 * c) >= 64 ? 4 : (T.se - 64 * c) / 16;
     } else {
-      const int i = 64 * (c - nsc);
+      const int i = 64 * (c - T.nsc);
       slot = p.s * p.b + i;
-      key = lbq * p.b + i;
-      nk = (nl - i) >= 64 ? 4 : (nl - i) / 16;
+      key = T.lbq * p.b + i;
+      nk = (T.nl - i) >= 64 ? 4 : (T.nl - i) / 16;
     }
   };
+  // barriers: Full[kQdStages], Empty[kQdStages], AccFull[2], AccFree[2]
   auto bar = [&](int i) { return sbase + kQdOffBar + 8 * i; };
+  const int kAccFull = 2 * kQdStages, kAccFree = kAccFull + 2;
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kQdOffTmemPtr);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kQdStages; ++i) {
       mbar_init(bar(i), 1);
       mbar_init(bar(kQdStages + i), 1);
     }
-    mbar_init(bar(2 * kQdStages), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(kAccFull + i), 1);
+      mbar_init(bar(kAccFree + i), 4);
+    }
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.ds_map);
     prefetch_tmap(&p.k_map);
   }
-  if (warp == 1) tmem_alloc<1>(smem_u32(tmem_ptr), 256);
+  if (warp == 1) tmem_alloc<1>(smem_u32(tmem_ptr), 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -488,73 +506,89 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_tc_kernel(const __grid_constant
     if (lane == 0) {
       const uint64_t pol = policy_evict_normal(), pol_k = policy_evict_last();
       uint32_t slot = 0, ph = 0;
-      for (int c = 0; c < nch; ++c) {
-        int sl, key, nk;
-        chunk(c, sl, key, nk);
-        mbar_wait(bar(kQdStages + slot), ph ^ 1);
-        mbar_arrive_expect_tx(bar(slot), kQdStage);
-        const uint32_t dst = sbase + slot * kQdStage;
-        tma_load_3d(dst, &p.ds_map, sl, r0, bi, bar(slot), pol);
-        tma_load_4d(dst + kQdA, &p.k_map, 0, key, 3 * slice, bi, bar(slot), pol_k);
-        if (++slot == kQdStages) {
-          slot = 0;
-          ph ^= 1;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile T = decode(t);
+        for (int c = 0; c < T.nch; ++c) {
+          int sl, key, nk;
+          chunk(T, c, sl, key, nk);
+          mbar_wait(bar(kQdStages + slot), ph ^ 1);
+          mbar_arrive_expect_tx(bar(slot), kQdStage);
+          const uint32_t dst = sbase + slot * kQdStage;
+          tma_load_3d(dst, &p.ds_map, sl, T.r0, T.bi, bar(slot), pol);
+          tma_load_4d(dst + kQdA, &p.k_map, 0, key, 3 * T.slice, T.bi, bar(slot), pol_k);
+          if (++slot == kQdStages) {
+            slot = 0;
+            ph ^= 1;
+          }
         }
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t id = idesc_bf16_f32(kRows, kQdN, false, true);
     uint32_t slot = 0, ph = 0;
-    for (int c = 0; c < nch; ++c) {
-      int sl, key, nk;
-      chunk(c, sl, key, nk);
-      mbar_wait(bar(slot), ph);
+    int n = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
+      const Tile T = decode(t);
+      const int ab = n & 1, use = n >> 1;
+      mbar_wait(bar(kAccFree + ab), (use & 1) ^ 1);
       tc_fence_after();
-      if (elect_one()) {
-        const uint32_t a = sbase + slot * kQdStage;
-        for (int k = 0; k < nk; ++k)
-          umma_bf16_1sm(tmem, sdesc_sw128(a + 32 * k, 16, 1024), sdesc_sw128(a + kQdA + 2048 * k, 8192, 1024), id,
-                        (c | k) != 0);
-        umma_commit_1sm(bar(kQdStages + slot));
+      for (int c = 0; c < T.nch; ++c) {
+        int sl, key, nk;
+        chunk(T, c, sl, key, nk);
+        mbar_wait(bar(slot), ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a = sbase + slot * kQdStage;
+          for (int k = 0; k < nk; ++k)
+            umma_bf16_1sm(tmem + kQdN * ab, sdesc_sw128(a + 32 * k, 16, 1024), sdesc_sw128(a + kQdA + 2048 * k, 8192, 1024),
+                          id, (c | k) != 0);
+          umma_commit_1sm(bar(kQdStages + slot));
+        }
+        __syncwarp();
+        if (++slot == kQdStages) {
+          slot = 0;
+          ph ^= 1;
+        }
       }
+      if (elect_one()) umma_commit_1sm(bar(kAccFull + ab));
       __syncwarp();
-      if (++slot == kQdStages) {
-        slot = 0;
-        ph ^= 1;
-      }
     }
-    if (elect_one()) umma_commit_1sm(bar(2 * kQdStages));
-    __syncwarp();
   } else if (warp >= 4) {
-    const int q = warp - 4, row = 32 * q + lane, r = r0 + row;
-    if (nch > 0) {
-      mbar_wait(bar(2 * kQdStages), 0);
+    const int q = warp - 4, row = 32 * q + lane;
+    int n = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
+      const Tile T = decode(t);
+      const int ab = n & 1, use = n >> 1, r = T.r0 + row;
+      mbar_wait(bar(kAccFull + ab), use & 1);
       tc_fence_after();
-    }
-    float* out = p.dq + ((int64_t)bi * p.rows + r) * kDqk + kQdN * slice;
-    for (int g = 0; g < kQdN / 32; ++g) {
-      uint32_t v[32];
-      if (nch > 0) {
-        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 32 * g, v);
-        tmem_wait_ld();
-      } else {
+      float* out = p.dq + ((int64_t)T.bi * p.rows + r) * kDqk + kQdN * T.slice;
+      for (int g = 0; g < kQdN / 32; ++g) {
+        uint32_t v[32];
+        if (T.nch > 0) {
+          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + kQdN * ab + 32 * g, v);
+          tmem_wait_ld();
+        } else {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = 0u;
-      }
-      if (r < p.rows) {
+          for (int c = 0; c < 32; ++c) v[c] = 0u;
+        }
+        if (r < p.rows) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 4)
-          *reinterpret_cast<float4*>(out + 32 * g + c) =
-              make_float4(__uint_as_float(v[c]) * p.scale, __uint_as_float(v[c + 1]) * p.scale,
-                          __uint_as_float(v[c + 2]) * p.scale, __uint_as_float(v[c + 3]) * p.scale);
+          for (int c = 0; c < 32; c += 4)
+            *reinterpret_cast<float4*>(out + 32 * g + c) =
+                make_float4(__uint_as_float(v[c]) * p.scale, __uint_as_float(v[c + 1]) * p.scale,
+                            __uint_as_float(v[c + 2]) * p.scale, __uint_as_float(v[c + 3]) * p.scale);
+        }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(bar(kAccFree + ab));
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<1>(tmem, 256);
+    tmem_dealloc<1>(tmem, 512);
   }
 }
 
@@ -678,6 +712,7 @@ cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq
   p.l = a.l;
   p.b = a.b;
   p.kv32 = (int32_t)((a.n_kv + 31) / 32 * 32);
+  p.batch = a.batch;
   p.scale = a.scale;
   {
     uint32_t l = 0;
@@ -687,8 +722,13 @@ cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq
   }
   cudaError_t e = cudaFuncSetAttribute(bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kQdSmem);
   if (e != cudaSuccess) return e;
-  const int64_t rt = ((int64_t)rows + kRows - 1) / kRows;
-  bwd_dq_tc_kernel<<<(unsigned)(a.batch * rt * 3), 256, kQdSmem, st>>>(p);
+  const int64_t rt = ((int64_t)rows + kRows - 1) / kRows, tiles = a.batch * rt * 3;
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  bwd_dq_tc_kernel<<<(unsigned)(tiles < sms ? tiles : sms), 256, kQdSmem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }
