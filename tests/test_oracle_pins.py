@@ -339,3 +339,21 @@ def test_backward_single_key_and_constant_v():
     dq, dk, dvv = oracle.attention_backward(q, pos, kc, vc, do, 0.5, 0, 1, 1, sparse=False)
     assert np.abs(dq).max() < 1e-12 and np.abs(dk).max() < 1e-12
     assert np.allclose(dvv.sum(0), do.astype(np.float64).sum(0), rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("sparse", [True, False])
+def test_backward_gradient_identities(sparse):
+    """Identities of the softmax gradient that hold at any size (also checked on the GPU at 8K,
+    tests/test_gpu_fullsize.py): sum_j P_rj = 1 gives sum_j dV_j = sum_r dO_r; sum_j dS_rj = D_r - D_r = 0
+    gives sum_j dK_j = 0. A dropped sink or window block, or a wrong D, breaks them."""
+    rng = np.random.default_rng(9)
+    pat = (1, 2, 4)
+    n_kv, dqk, dv = 40, 7, 5
+    pos = np.repeat(np.arange(n_kv), 2)  # two heads per position
+    q = rng.standard_normal((len(pos), dqk)).astype(np.float32)
+    k = rng.standard_normal((n_kv, dqk)).astype(np.float32)
+    v = rng.standard_normal((n_kv, dv)).astype(np.float32)
+    do = rng.standard_normal((len(pos), dv)).astype(np.float32)
+    dq, dk, dvv = oracle.attention_backward(q, pos, k, v, do, 0.6, *pat, sparse=sparse)
+    assert np.abs(dvv.sum(0) - do.astype(np.float64).sum(0)).max() <= 1e-12 * max(1.0, np.abs(dvv).sum())
+    assert np.abs(dk.sum(0)).max() <= 1e-12 * max(1.0, np.abs(dk).sum())
