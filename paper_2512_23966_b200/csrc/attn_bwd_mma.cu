@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(256) bwd_sink_reduce_kernel(MP p) {
 }
 
 int sink_splits(const AttnProblem& a) {
-  if (!a.sparse) return 1;
+  if (!a.sparse || a.s == 0 || a.n_kv == 0) return 1;  // no sink tiles: nothing to split
   const int64_t win = (int64_t)a.l * a.b;
   int64_t n = (a.n_q + win - 1) / win;
   return (int)(n < 1 ? 1 : n > 64 ? 64 : n);

@@ -103,6 +103,7 @@ def test_seqpar_validation():
     (2, 8192, (1, 7, 128), 2 * 8192 * 64 * 4 + 2 * 4 * 10 * 32 * 1088 * 4 + 2 * 2 * 8192 * 64 * 1024),
     (1, 512, (1, 7, 128), 512 * 64 * 4 + 2 * 512 * 64 * 1024),                        # one split: no partials
     (1, 1024, (2, 1, 128), 1024 * 64 * 4 + 8 * 8 * 32 * 1088 * 4 + 2 * 1024 * 64 * 384),  # two sink blocks, 8 splits
+    (1, 1024, (0, 2, 128), 1024 * 64 * 4 + 2 * 1024 * 64 * 256),  # no sink blocks: no partials
 ])
 def test_backward_workspace_size(B, n, pat, want):
     """loza_workspace_size(LOZA_WS_BACKWARD) is what attention_backward checks against (host logic only)."""
