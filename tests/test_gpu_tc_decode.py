@@ -27,7 +27,7 @@ def _oracle_decode(qs, ks, bi, L, pattern, sparse=True):
     return oracle.attend(qr, kf, kf[:, :D_V], SCALE)
 
 
-@pytest.mark.parametrize("pattern", [(1, 7, 128), (1, 2, 128), (2, 3, 256)])
+@pytest.mark.parametrize("pattern", [(1, 7, 128), (1, 2, 128), (2, 3, 256), (0, 3, 128)])
 @pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
 def test_ssa_decode_ragged(pattern, out_dtype):
     seq = [1, 100, 128, 129, 1023, 1024, 1025, 2048, 3000, 4096]

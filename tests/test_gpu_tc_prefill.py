@@ -63,6 +63,18 @@ def test_ssa_prefill_small(kind, out_dtype):
     _check_rows(o, lse, qs, ks, [0, 1, 63, 127, 128, 255, 256, 300, 383, 384, 511, 640, 1000, 1022, 1023], pat, True)
 
 
+def test_ssa_prefill_no_sink_blocks():
+    """s = 0 (local window only, PAPER.md's SSA with no sink): the tcgen05 prefill against the oracle, LSE too."""
+    n, H, pat = 1024, 64, (0, 3, 128)
+    qs, ks = _specs(3, 1, n, H)
+    q, kv = empty_filled(qs), empty_filled(ks)
+    lse = torch.full((1, H, n), float("nan"), device="cuda")
+    o = loza.ssa_prefill(q, kv, pattern=pat, scale=SCALE, lse=lse, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert torch.isfinite(o).all()
+    _check_rows(o, lse, qs, ks, [0, 127, 128, 383, 384, 385, 511, 700, 1023], pat, True)
+
+
 def test_ssa_paper_pattern_and_window_degeneracy():
     """(1,7,128) at n=2048 vs oracle; and n <= (s+l)b => SSA == full attention (north star)."""
     n, H = 2048, 64
