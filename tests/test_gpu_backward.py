@@ -142,6 +142,7 @@ def test_backward_tiled_fp32_h8(sparse, causal, q0):
     (True, True, 0, 24, 300, (1, 1, 128), 1, True),     # H = 24: tcgen05 keys, dQ by the warp-MMA row kernel
     (True, True, 0, 128, 300, (1, 1, 128), 1, True),    # H = 128: one token per 128-row dQ tile
     (True, True, 0, 8, 400, (0, 2, 128), 1, True),      # no sink blocks (s = 0): no sink tiles or splits
+    (True, True, 0, 16, 1280, (1, 2, 256), 1, False),   # b = 256: 8 key tiles per block, 2 splits
 ])
 def test_backward_mla_mma(sparse, causal, q0, H, n, pat, B, ofwd):
     """The tensor-core backward (SSA: D, tcgen05 key kernel writing dS rows, tcgen05 dQ = dS K; full attention:
