@@ -34,7 +34,7 @@ constexpr int kKBytes = 9 * kKeys * 128;       // 36 KB: [9 chunks][32 keys][64]
 constexpr int kPBytes = kRows * 64;            // [128 rows][32 keys] bf16, SWIZZLE_64B
 constexpr int kOffRing = 0;
 constexpr int kOffK = kOffRing + kStages * kPairBytes;
-constexpr int kOffP = kOffK + kKBytes;         // 2 buffers
+constexpr int kOffP = kOffK + kKBytes;         // kPBufs buffers each for P and dS
 constexpr int kOffDS = kOffP + kPBufs * kPBytes;
 constexpr int kOffBar = kOffDS + kPBufs * kPBytes;
 constexpr int kBarFull = 0, kBarEmpty = kStages, kBarK = 2 * kStages, kBarSFull = kBarK + 1,
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
           ph ^= 1;
         }
       };
-      // S/dP of tile t + 1 are issued before dK^T/dV^T of tile t (S/dP and P/dS double-buffered), so the
+      // S/dP of tile t + 1 are issued before dK^T/dV^T of tile t (S/dP double-buffered in TMEM), so the
       // tensor pipe works while the four P/dS warps process tile t
       auto issue_sdp = [&](int tc) {
         const int buf = tc & 1, use = tc >> 1;
