@@ -194,28 +194,75 @@ loza_status_t ssa_ring_append(const void* rows, int64_t rows_stride_b, int64_t r
 loza_status_t ssa_decode_ring(const loza_attn_args_t* args, const int32_t* seq_lens_dev, loza_pattern_t pattern,
                               loza_stream_t stream);
 
-/* Sequence-parallel SSA prefill (north star; "uniform compute across
+/* Sequence-parallel SSA prefill (north star; SURVEY.md §8 a10 / e; "uniform compute across
  * all ranks"). Rank r of `world` owns the contiguous, block-aligned shard of one
  * sequence at positions [q_start, q_start + n_local) with n_local = args->n_q,
  * q_start = r * n_local (equal shards), and k/v holding exactly the shard's own
  * rows (args->n_kv == n_local; k row 0 = position q_start; rows contiguous).
- * One NCCL group on `stream`: rank 0 broadcasts its first s*b KV rows (the sink
- * blocks), rank r sends its last (l-1)*b KV rows to rank r+1 and receives the
- * halo from rank r-1; then the SSA prefill of the shard runs over the segmented
- * KV [sink | halo | shard]. The output stays sharded (o/lse hold the shard's rows).
+ * The exchange is the plan loza_seqpar_plan returns, in two NCCL groups:
+ *   1. on `stream`: rank 0 broadcasts its first s*b KV rows (the sink blocks);
+ *   2. on a library-owned communication stream forked from `stream`: rank r sends
+ *      its last (l-1)*b KV rows to rank r+1 and receives the halo from rank r-1.
+ * The shard's query blocks [l-1, n_local/b) need only [sink | shard] and run on
+ * `stream` while the halo is in flight; the first l-1 blocks (the only ones that
+ * reach into the halo) run after it, over the segmented KV [sink | halo | shard].
+ * The output stays sharded (o/lse hold the shard's rows); no gather, no LSE merge.
+ * Splitting the launch does not change any result: every 128-row unit is computed
+ * the same way in either launch (tests: bitwise equal to the one-GPU ssa_prefill).
  * Requires n_local % b == 0 and n_local >= max(s, l-1) * b (LOZA_ERR_SHAPE).
  * `comm` (an ncclComm_t of `world` ranks) may be NULL when world == 1.
- * ws: loza_workspace_size(LOZA_WS_SEQPAR, args, pattern, world) bytes. */
+ * ws: loza_workspace_size(LOZA_WS_SEQPAR, args, pattern, world) bytes.
+ * The communication stream and its two events are created once per (host thread,
+ * device) and reused (the only state the library keeps). */
 loza_status_t ssa_seqpar_prefill(const loza_attn_args_t* args, loza_pattern_t pattern, loza_nccl_comm_t comm,
                                  int32_t rank, int32_t world, void* ws, size_t ws_bytes, loza_stream_t stream);
 
-/* Test hook ("virtual ranks"): ssa_seqpar_prefill with the NCCL exchange replaced
- * by device-to-device copies from the other shards' k/v on this GPU (rank0_k/v:
- * rank 0's shard base; prev_k/v: rank r-1's shard base; ignored for rank 0). */
+/* One transfer of the sequence-parallel exchange (host description, no device work). */
+enum { LOZA_XFER_BCAST = 0, LOZA_XFER_SEND = 1, LOZA_XFER_RECV = 2 };
+typedef struct {
+  int32_t op;         /* LOZA_XFER_*; BCAST is group 1 (sink), SEND / RECV group 2 (halo) */
+  int32_t peer;       /* BCAST: root rank (0); SEND: destination rank; RECV: source rank */
+  int32_t batch;      /* sequence index b in [0, B) */
+  int32_t tensor;     /* 0 = k rows, 1 = v rows (only when v does not alias k) */
+  int64_t src_row;    /* first row moved, as a row index of the SENDER's shard (BCAST: the root's) */
+  int64_t rows;       /* rows moved */
+  int64_t row_elems;  /* elements per row (d_qk for k, d_v for v) */
+  int64_t ws_offset;  /* byte offset of the destination in ws; -1 = none (the BCAST root keeps its rows) */
+} loza_xfer_t;
+
+/* The exchange plan of rank `rank` (host only; callable without a GPU): writes up to max_out entries to
+ * out and returns their number (>= 0; the full count even when max_out is smaller), or -(status) if the
+ * arguments are invalid for ssa_seqpar_prefill (see loza_last_error()). Entries are listed in issue order. */
+int32_t loza_seqpar_plan(const loza_attn_args_t* args, loza_pattern_t pattern, int32_t rank, int32_t world,
+                         loza_xfer_t* out, int32_t max_out);
+
+/* The segmented KV view rank `rank` attends over after the exchange (host only): for segment i < the returned
+ * count (1..3), seg_out[6*i + 0..5] = (pos_begin, pos_end, byte offset in ws of its k rows for batch 0, same
+ * for its v rows, k batch stride in bytes, v batch stride in bytes); offsets are -1 for the shard's own k / v
+ * (then the strides are the args' ones). Returns -(status) on invalid arguments. Key at absolute position j
+ * of batch b lives in the segment with pos_begin <= j < pos_end, at row j - pos_begin. */
+int32_t loza_seqpar_segments(const loza_attn_args_t* args, loza_pattern_t pattern, int32_t rank, int32_t world,
+                             int64_t* seg_out);
+
+/* Test hook ("virtual ranks"): ssa_seqpar_prefill with every RECV / BCAST of the
+ * plan done by a device-to-device copy from the other shards' k/v on this GPU
+ * (rank0_k/v: rank 0's shard base; prev_k/v: rank r-1's shard base; ignored for
+ * rank 0); same streams, same split launch. */
 loza_status_t loza_seqpar_prefill_local(const loza_attn_args_t* args, loza_pattern_t pattern, int32_t rank,
                                         int32_t world, const void* rank0_k, const void* rank0_v,
                                         const void* prev_k, const void* prev_v, void* ws, size_t ws_bytes,
                                         loza_stream_t stream);
+
+/* Test hook ("NCCL loopback"): like loza_seqpar_prefill_local, but the plan's transfers go through NCCL on
+ * a ONE-rank communicator `comm` (e.g. torch's ProcessGroupNCCL at world size 1): each BCAST becomes
+ * ncclBroadcast(rank 0's rows -> ws, root 0), each RECV an ncclSend(rank r-1's rows, peer 0) +
+ * ncclRecv(ws, peer 0) pair in the same group (SEND entries are the next virtual rank's RECVs). Exercises
+ * the NCCL calls, counts, datatypes and offsets of ssa_seqpar_prefill on one GPU without cross-process
+ * waits. */
+loza_status_t loza_seqpar_prefill_loopback(const loza_attn_args_t* args, loza_pattern_t pattern,
+                                           loza_nccl_comm_t comm, int32_t rank, int32_t world,
+                                           const void* rank0_k, const void* rank0_v, const void* prev_k,
+                                           const void* prev_v, void* ws, size_t ws_bytes, loza_stream_t stream);
 
 /* Test hook for the integer prologue: for the query blocks of
  * queries [q_start, q_start + n_q) (q_start % b == 0), local block qb:

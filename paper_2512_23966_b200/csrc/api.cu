@@ -74,7 +74,7 @@ loza_status_t make_problem(const loza_attn_args_t* a, bool sparse, loza_pattern_
   p->s = sparse ? pat.sink_blocks : 0; p->l = sparse ? pat.local_blocks : 1; p->b = sparse ? pat.block_size : 1;
   p->q = a->q; p->q_sb = a->q_stride_b; p->q_st = a->q_stride_tok; p->q_sh = a->q_stride_head;
   p->o = a->o; p->o_sb = a->o_stride_b; p->o_st = a->o_stride_tok; p->o_sh = a->o_stride_head;
-  p->lse = a->lse; p->seq_lens = seq_lens;
+  p->lse = a->lse; p->lse_sh = a->n_q; p->seq_lens = seq_lens;
   p->kv.nseg = 1;
   p->kv.seg[0] = KvSeg{0, a->n_kv, a->k, a->v, a->k_stride_b, a->k_stride_tok, a->v_stride_b, a->v_stride_tok};
   return LOZA_OK;

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) attn_simt_kernel(const At
       }
     }
   }
-  if (p.lse && lane == 0) p.lse[((int64_t)bi * p.heads + h) * p.n_q + i] = st.m + logf(st.l);
+  if (p.lse && lane == 0) p.lse[((int64_t)bi * p.heads + h) * p.lse_sh + i] = st.m + logf(st.l);
 }
 
 }  // namespace

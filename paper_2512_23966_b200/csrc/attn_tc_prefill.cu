@@ -125,6 +125,7 @@ struct PrefillParams {
   int64_t o_sb;
   int32_t out_bf16;
   float* lse;
+  int64_t lse_sh;  // lse head stride (elements)
   int64_t units_per_batch, total_units;
   // fused calibration forward (Eq. 3 in the epilogue; CalibArgs): o receives o_hat
   const uint8_t* o_full;   // NULL: plain prefill
@@ -843,7 +844,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       }
       if (p.lse && row_ok && q4 == 0) {
         const int64_t h = row_g % p.heads, tl_ = row_g / p.heads;
-        p.lse[((int64_t)U.bi * p.heads + h) * p.n_q + tl_] = (m_used + __log2f(ltot)) * ln2;
+        p.lse[((int64_t)U.bi * p.heads + h) * p.lse_sh + tl_] = (m_used + __log2f(ltot)) * ln2;
       }
       g += U.n_tiles;
     }
@@ -895,6 +896,7 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
   p.o_sb = a.o_sb;
   p.out_bf16 = a.out_bf16;
   p.lse = a.lse;
+  p.lse_sh = a.lse_sh;
   if (a.calib) {
     if (!encode_3d(&p.of_map, a.calib->o_full, kDv, (uint64_t)a.n_q * a.heads, a.batch, kDv, a.o_sb, 64))
       return cudaErrorInvalidValue;

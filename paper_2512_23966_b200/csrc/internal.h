@@ -45,6 +45,8 @@ struct AttnProblem {
   void* o;
   int64_t o_sb, o_st, o_sh;
   float* lse;
+  int64_t lse_sh;             // lse [B, H, *] head stride in elements (make_problem: n_q; a sub-range launch
+                              // of a longer problem keeps the longer n_q)
   const int32_t* seq_lens;  // non-NULL => decode (one query at seq_len-1)
   KvView kv;
   const CalibArgs* calib = nullptr;  // non-NULL => fused blend epilogue (bf16 SSA prefill only)

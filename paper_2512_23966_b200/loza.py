@@ -25,8 +25,8 @@ STATUS = {0: "LOZA_OK", 1: "LOZA_ERR_INVALID", 2: "LOZA_ERR_SHAPE", 3: "LOZA_ERR
 PAPER_PATTERN = (1, 7, 128)  # (s, l, b)
 EXPORTS = ["ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_prefill_blend", "attention_backward",
            "ssa_prefill_mha", "ssa_ring_append",
-           "ssa_decode_ring", "ssa_seqpar_prefill",
-           "loza_seqpar_prefill_local", "ssa_select_blocks", "loza_workspace_size", "loza_status_string",
+           "ssa_decode_ring", "ssa_seqpar_prefill", "loza_seqpar_plan", "loza_seqpar_segments",
+           "loza_seqpar_prefill_local", "loza_seqpar_prefill_loopback", "ssa_select_blocks", "loza_workspace_size", "loza_status_string",
            "loza_last_error", "loza_kernel_launches", "loza_num_sms"]
 
 
@@ -53,6 +53,15 @@ class AttnArgs(ctypes.Structure):
                 ("o_stride_head", ctypes.c_int64), ("lse", ctypes.c_void_p)]
 
 
+class Xfer(ctypes.Structure):
+    """loza_xfer_t: one transfer of the sequence-parallel exchange plan."""
+    _fields_ = [("op", ctypes.c_int32), ("peer", ctypes.c_int32), ("batch", ctypes.c_int32),
+                ("tensor", ctypes.c_int32), ("src_row", ctypes.c_int64), ("rows", ctypes.c_int64),
+                ("row_elems", ctypes.c_int64), ("ws_offset", ctypes.c_int64)]
+
+
+XFER_BCAST, XFER_SEND, XFER_RECV = 0, 1, 2
+
 _lib = None
 
 
@@ -76,6 +85,11 @@ def lib():
         L.ssa_prefill_mha.argtypes = [P(AttnArgs), I64, I64, I32, Pattern, V]
         L.ssa_seqpar_prefill.argtypes = [P(AttnArgs), Pattern, V, I32, I32, V, SZ, V]
         L.loza_seqpar_prefill_local.argtypes = [P(AttnArgs), Pattern, I32, I32, V, V, V, V, V, SZ, V]
+        L.loza_seqpar_prefill_loopback.argtypes = [P(AttnArgs), Pattern, V, I32, I32, V, V, V, V, V, SZ, V]
+        L.loza_seqpar_plan.argtypes = [P(AttnArgs), Pattern, I32, I32, P(Xfer), I32]
+        L.loza_seqpar_plan.restype = I32
+        L.loza_seqpar_segments.argtypes = [P(AttnArgs), Pattern, I32, I32, P(I64)]
+        L.loza_seqpar_segments.restype = I32
         L.ssa_select_blocks.argtypes = [I64, I64, Pattern, I32, V, V, V]
         L.loza_workspace_size.argtypes = [I32, P(AttnArgs), Pattern, I32]
         L.loza_workspace_size.restype = SZ
@@ -84,7 +98,7 @@ def lib():
         L.loza_kernel_launches.restype = ctypes.c_uint64
         L.loza_num_sms.restype = I32
         for fn in ("ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_seqpar_prefill",
-                   "loza_seqpar_prefill_local", "ssa_select_blocks"):
+                   "loza_seqpar_prefill_local", "loza_seqpar_prefill_loopback", "ssa_select_blocks"):
             getattr(L, fn).restype = S
         _lib = L
     return _lib
@@ -440,4 +454,69 @@ def ssa_seqpar_prefill_local(q_shard, k_shard, v=None, pattern=PAPER_PATTERN, sc
     _check(lib().loza_seqpar_prefill_local(ctypes.byref(a), _pattern(pattern), rank, world, ptr(rank0_k),
                                            ptr(rank0_v), ptr(prev_k), ptr(prev_v), V(ws.data_ptr()), need,
                                            _stream(stream)))
+    return o
+
+
+def seqpar_host_args(n_local: int, rank: int, *, batch=1, heads=64, d_qk=576, d_v=512, alias=True,
+                     dtype=LOZA_BF16) -> AttnArgs:
+    """AttnArgs describing rank `rank`'s shard for the host-only plan queries (no tensors: the plan and the
+    segments depend on shapes, strides and whether v aliases k only)."""
+    a = AttnArgs()
+    a.batch, a.n_q, a.heads, a.d_qk, a.d_v = batch, n_local, heads, d_qk, d_v
+    a.n_kv, a.q_start = n_local, rank * n_local
+    a.in_dtype = a.out_dtype = dtype
+    a.softmax_scale, a.causal = 1.0, 1
+    a.q_stride_b, a.q_stride_tok, a.q_stride_head = n_local * heads * d_qk, heads * d_qk, d_qk
+    a.k = 4096  # stand-in addresses: only k == v (MLA aliasing) matters to the plan
+    a.k_stride_b, a.k_stride_tok = n_local * d_qk, d_qk
+    a.v = a.k if alias else 8192
+    a.v_stride_b, a.v_stride_tok = (n_local * d_qk, d_qk) if alias else (n_local * d_v, d_v)
+    a.o_stride_b, a.o_stride_tok, a.o_stride_head = n_local * heads * d_v, heads * d_v, d_v
+    return a
+
+
+def seqpar_plan(a: AttnArgs, pattern, rank: int, world: int):
+    """The exchange plan (list of dicts, issue order) ssa_seqpar_prefill executes for this rank."""
+    n = lib().loza_seqpar_plan(ctypes.byref(a), _pattern(pattern), rank, world, None, 0)
+    if n < 0:
+        _check(-n)
+    buf = (Xfer * max(n, 1))()
+    lib().loza_seqpar_plan(ctypes.byref(a), _pattern(pattern), rank, world, buf, n)
+    return [{f: getattr(buf[i], f) for f, _ in Xfer._fields_} for i in range(n)]
+
+
+def seqpar_segments(a: AttnArgs, pattern, rank: int, world: int):
+    """Segments of the KV view after the exchange: dicts with pos_begin, pos_end, k_off, v_off (ws byte offsets
+    for batch 0, -1 = the shard's own rows), k_sb, v_sb (batch strides in bytes)."""
+    out = (ctypes.c_int64 * 18)()
+    n = lib().loza_seqpar_segments(ctypes.byref(a), _pattern(pattern), rank, world, out)
+    if n < 0:
+        _check(-n)
+    keys = ("pos_begin", "pos_end", "k_off", "v_off", "k_sb", "v_sb")
+    return [{k: out[6 * i + j] for j, k in enumerate(keys)} for i in range(n)]
+
+
+def ssa_seqpar_prefill_loopback(q_shard, k_shard, v=None, pattern=PAPER_PATTERN, scale=None, *, rank: int,
+                                world: int, comm_ptr: int, rank0_k=None, rank0_v=None, prev_k=None, prev_v=None,
+                                d_v=512, out=None, lse=None, out_dtype=None, stream=None):
+    """Test hook: the exchange through NCCL on a one-rank communicator (comm_ptr), virtual ranks on one GPU."""
+    k_shard, v = _split_kv(k_shard, v, d_v)
+    scale = default_scale(q_shard.shape[-1]) if scale is None else scale
+    n_local = _q4(q_shard).shape[1]
+    o = out if out is not None else _alloc_out(q_shard, v.shape[-1], out_dtype)
+    a = make_args(q_shard, k_shard, v, o, scale=scale, q_start=rank * n_local, lse=lse)
+    need = int(lib().loza_workspace_size(LOZA_WS_SEQPAR, ctypes.byref(a), _pattern(pattern), world))
+    s = torch.cuda.current_stream() if stream is None else stream
+    with torch.cuda.stream(s):
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=q_shard.device)
+    V = ctypes.c_void_p
+
+    def ptr(t):
+        return V(t.data_ptr() if t is not None else 0)
+    if v.data_ptr() == k_shard.data_ptr():
+        rank0_v = rank0_k if rank0_v is None else rank0_v
+        prev_v = prev_k if prev_v is None else prev_v
+    _check(lib().loza_seqpar_prefill_loopback(ctypes.byref(a), _pattern(pattern), V(comm_ptr), rank, world,
+                                              ptr(rank0_k), ptr(rank0_v), ptr(prev_k), ptr(prev_v),
+                                              V(ws.data_ptr()), need, _stream(stream)))
     return o
