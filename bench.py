@@ -5,8 +5,13 @@ Contract (one JSON line on rank 0):
         (s,l,b) = (1,7,128), bf16 in / fp32 accumulate / bf16 out; value = tokens/s. The other §8 rows
         (full-attention comparator at the same shape, decode B64 at 128K/512K/1M, blend 8K) are measured in
         the same run and reported under "rows".
-  N>1 : sequence-parallel SSA prefill (configs[4] path): each rank owns a 32768-token shard of one
-        (32768*N)-token sequence, NCCL halo + sink exchange; weak scaling; value = total tokens / max-rank time.
+        The 1M-token SSA prefill on this one GPU (configs[4] at N=1, the base of the strong-scaling curve) is the
+        row "ssa_prefill_1m".
+  N>1 : sequence-parallel SSA prefill of ONE 1,048,576-token sequence (configs[4]): rank r owns tokens
+        [r*2^20/N, (r+1)*2^20/N), NCCL sink broadcast + halo exchange (ssa_seqpar_prefill); strong scaling;
+        value = 2^20 tokens / max-rank step time. `python bench.py --gpus N` re-launches itself under
+        torch.distributed.run (one process per GPU) when WORLD_SIZE is not set, and fails loudly when the node
+        has fewer than N GPUs or WORLD_SIZE disagrees with --gpus.
   --impl reference : the fp64 CPU oracle (oracle/) timed on a bounded sample of the same workload.
 """
 from __future__ import annotations
@@ -28,21 +33,20 @@ sys.path.insert(0, ROOT)
 PATTERN = (1, 7, 128)
 D_QK, D_V, H = 576, 512, 64
 N_PREFILL = 32768
+N_SP = 1 << 20  # configs[4]: the sequence-parallel prefill's sequence length (all N)
 FLOP_PER_PAIR = 2 * (D_QK + D_V) * H  # 139,264
 
 
 def ssa_pairs(n, s, l, b, q_start=0):
-    """Unmasked (query, key) pairs of SSA for queries [q_start, q_start+n) (closed form summed per block)."""
+    """Unmasked (query, key) pairs of SSA for queries [q_start, q_start+n): per query block, every earlier
+    selected key block (sink blocks kb < s, local blocks qb-l+1 <= kb < qb) gives b keys to each query and the
+    own block gives p - qb*b + 1 (DESIGN R2-R5)."""
     tot = 0
     for qb in range(q_start // b, (q_start + n + b - 1) // b):
         lo, hi = max(qb * b, q_start), min((qb + 1) * b, q_start + n)
-        sink_blocks = [kb for kb in range(min(s, qb + 1))]
-        loc = [kb for kb in range(max(s, qb - l + 1), qb + 1)]
-        for p in range(lo, hi):
-            cnt = 0
-            for kb in sink_blocks + loc:
-                cnt += max(0, min((kb + 1) * b, p + 1) - kb * b)
-            tot += cnt
+        prev = len(set(range(min(s, qb))) | set(range(max(0, qb - l + 1), qb)))
+        a0, a1 = lo - qb * b + 1, hi - qb * b  # own-block counts of the first / last query
+        tot += (hi - lo) * b * prev + (a0 + a1) * (hi - lo) // 2
     return tot
 
 
@@ -123,6 +127,29 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
 
 
+def metric_name(world):
+    if world == 1:
+        return "SSA prefill tokens/s (B1 H64 n32768 MLA 576/512, (s,l,b)=(1,7,128)); % tensor roofline"
+    return ("sequence-parallel SSA prefill tokens/s (B1 H64 n1048576 MLA 576/512, (s,l,b)=(1,7,128), "
+            f"{world} ranks); % tensor roofline")
+
+
+def clock_normalized(achieved_tf, sm_mhz, sms=148, flop_per_clk_sm=8192):
+    """Achieved algorithmic TFLOP/s over the dense bf16 tcgen05 rate at the SM clock measured during the run
+    (148 SMs x 8192 FLOP/clk/SM, B200_PROFILING.md): the tensor-pipe fraction independent of the clock."""
+    if not sm_mhz:
+        return None
+    return achieved_tf / (sms * flop_per_clk_sm * sm_mhz * 1e6 / 1e12)
+
+
+def _host_available():
+    try:
+        import psutil
+        return float(psutil.virtual_memory().available)
+    except Exception:  # noqa: BLE001
+        return 0.0
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def _time_events(fn, iters, warmup, flush=None, stream=None):
     """Per-iteration device times (ms) with CUDA events on the launching stream; L2 flushed between iterations."""
@@ -162,8 +189,8 @@ def run_gpu(args):
     peaks = measured_peaks()
     scale = loza.default_scale(D_QK)
     s, l, b = PATTERN
-    n_local = N_PREFILL
-    n_total = n_local * world
+    n_total = N_PREFILL if world == 1 else N_SP
+    n_local = n_total // world
 
     # inputs (generated on the device; seed 0, D1 distribution)
     qs = Spec(seed=0, tensor_id=TID_Q, batch=1, n=n_total, heads=H, d=D_QK)
@@ -216,10 +243,13 @@ def run_gpu(args):
         torch.cuda.synchronize()
     launches = loza.kernel_launches() - launches0
     t_ms = float(np.mean(per_step))
+    rank_ms = [t_ms]
     if world > 1:
         tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+        allt = [torch.empty_like(tt) for _ in range(world)]
+        dist.all_gather(allt, tt)
+        rank_ms = [float(x.item()) for x in allt]
+        t_ms = max(rank_ms)
     tokens = n_total
     value = tokens / (t_ms * 1e-3)
     pairs = ssa_pairs(n_local, s, l, b, q_start=rank * n_local)
@@ -312,7 +342,11 @@ def run_gpu(args):
     # ---- e2e at N > 1: every rank uploads its shard (pinned host buffers), runs the sequence-parallel
     # prefill through the public API (NCCL sink/halo exchange inside), downloads its output shard; K steps
     # back to back, max over ranks (the same collective sequence on every rank)
-    if world > 1 and not args.no_e2e:
+    e2e_host_bytes = world * (q.numel() + kv.numel() + o.numel()) * 2  # every rank's pinned shard buffers
+    if world > 1 and not args.no_e2e and _host_available() < 1.25 * e2e_host_bytes:
+        e2e = {"unavailable": f"needs {e2e_host_bytes / 1e9:.0f} GB of pinned host memory for the {world} ranks' "
+                              f"shards, {_host_available() / 1e9:.0f} GB available"}
+    elif world > 1 and not args.no_e2e:
         try:
             qh = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
             kh = torch.empty(kv.shape, dtype=kv.dtype, pin_memory=True)
@@ -351,22 +385,27 @@ def run_gpu(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.cpu_seconds)
+        cpu = cpu_baseline(args.cpu_seconds, n_total)
 
     if rank == 0:
         frac = achieved_tf / peaks["bf16_tflops"]
+        csum = clk.summary()
         line = {
-            "metric": "SSA prefill tokens/s (B1 H64 n32768 MLA 576/512, (s,l,b)=(1,7,128)); % tensor roofline",
+            "metric": metric_name(world),
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+            "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (counter-based N(0,1)-like, seed 0; inputs/gen.py)",
-            "config": {"workload": "ssa_prefill_32k" if world == 1 else f"ssa_seqpar_prefill_{world}x32k",
+            "config": {"workload": "ssa_prefill_32k" if world == 1 else "ssa_seqpar_prefill_1m",
                        "batch": 1, "seq_len": n_total, "tokens_per_gpu": n_local, "heads": H, "d_qk": D_QK,
                        "d_v": D_V, "pattern": list(PATTERN), "softmax_scale": scale,
                        "parallelism": f"sp{world}" if world > 1 else "single",
-                       "l2": "flushed between timed steps (256 MB write)"},
+                       "l2": "flushed between timed steps (256 MB write)" if world == 1 else
+                             "flushed between timed steps (256 MB write); per-rank inputs (>= 9.7 GB) exceed L2"},
+            "per_rank_ms": rank_ms,
             "roofline": {"bound": "tensor", "kernel": "prefill_tc_kernel", "achieved": achieved_tf,
                          "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": frac,
+                         "clock_normalized_frac": clock_normalized(achieved_tf, csum.get("sm_mhz")),
                          "traffic": ncu_traffic("prefill_tc_kernel") if world == 1 else None,
                          "traffic_note": "DRAM bytes per launch from the committed ncu capture (profiles/); "
                                          "algorithmic Q+KV+O bytes = 4.60e9",
@@ -374,7 +413,7 @@ def run_gpu(args):
                          "peak_source": peaks["source"] + " bf16_tflops (burst)",
                          "frac_vs_sustained": achieved_tf / peaks["bf16_tflops_sustained"]
                          if peaks.get("bf16_tflops_sustained") else None},
-            "clocks": clk.summary(),
+            "clocks": csum,
             "gpu_launches": int(launches),
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -399,6 +438,12 @@ def extra_rows(args, q, kv, o, flush, peaks):
     out = {}
     scale = loza.default_scale(D_QK)
     dev = q.device
+    if not args.no_1m:
+        try:
+            out["ssa_prefill_1m"] = prefill_1m_row(peaks, flush)
+        except Exception as e:  # noqa: BLE001 -- reported in the line
+            out["ssa_prefill_1m"] = {"error": repr(e)[:300]}
+        torch.cuda.empty_cache()
     # full-attention prefill at the same shape
     t = _time_events(lambda: loza.full_attn_ref(q, kv, scale=scale, out=o), 2, 1, flush)
     fl = full_pairs(N_PREFILL) * FLOP_PER_PAIR
@@ -488,6 +533,44 @@ def extra_rows(args, q, kv, o, flush, peaks):
         except Exception as e:  # report, do not hide: the headline line still prints
             out["decode"] = {"error": repr(e)[:300]}
     return out
+
+
+def prefill_1m_row(peaks, flush, steps=5, warmup=2):
+    """configs[4] on ONE GPU: SSA prefill of a 1,048,576-token sequence (B1 H64 MLA 576/512, (1,7,128)): Q 77.3 GB,
+    O 68.7 GB bf16 (the base of the strong-scaling curve of the N>1 lines; parity: tests/test_gpu_1m.py).
+    A step is ~0.14 s of continuous tensor work, so the clock settles under the power cap: the roofline is
+    given against the SUSTAINED bf16 peak (MEASURED_PEAKS.json) and clock-normalised."""
+    import torch
+
+    from inputs import TID_K, TID_Q, Spec
+    from inputs.device import empty_filled
+    from paper_2512_23966_b200 import loza
+    n = N_SP
+    need = n * H * (D_QK + D_V) * 2 + n * D_QK * 2
+    free = torch.cuda.mem_get_info()[0]
+    if free < need + (1 << 30):
+        return {"skipped": f"needs {need / 1e9:.1f} GB of device memory, {free / 1e9:.1f} GB free"}
+    q = empty_filled(Spec(seed=0, tensor_id=TID_Q, batch=1, n=n, heads=H, d=D_QK))
+    kv = empty_filled(Spec(seed=0, tensor_id=TID_K, batch=1, n=n, heads=1, d=D_QK))
+    o = torch.empty((1, n, H, D_V), dtype=torch.bfloat16, device=q.device)
+    scale = loza.default_scale(D_QK)
+    with ClockSampler(q.device.index) as clk:
+        t = _time_events(lambda: loza.ssa_prefill(q, kv, pattern=PATTERN, scale=scale, out=o), steps, warmup, flush)
+    del q, kv, o
+    ms = float(np.mean(t))
+    fl = ssa_pairs(n, *PATTERN) * FLOP_PER_PAIR
+    tf = fl / (ms * 1e-3) / 1e12
+    c = clk.summary()
+    sus = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
+    return {"ms": ms, "ms_all": t, "tokens_per_s": n / (ms * 1e-3),
+            "roofline": {"bound": "tensor", "kernel": "prefill_tc_kernel", "achieved": tf, "unit": "TFLOP/s",
+                         "peak": sus, "frac": tf / sus, "peak_source": peaks["source"] + " bf16_tflops_sustained",
+                         "frac_vs_burst": tf / peaks["bf16_tflops"],
+                         "clock_normalized_frac": clock_normalized(tf, c.get("sm_mhz")),
+                         "algorithmic_flop_per_launch": fl, "pairs_per_launch": ssa_pairs(n, *PATTERN)},
+            "clocks": c, "steps": steps, "warmup": warmup,
+            "config": {"workload": "ssa_prefill_1m", "batch": 1, "seq_len": n, "heads": H, "pattern": list(PATTERN),
+                       "l2": "inputs (146 GB) exceed L2; flushed between steps anyway"}}
 
 
 def decode_rows(args, peaks, flush):
@@ -586,31 +669,41 @@ def decode_rows(args, peaks, flush):
 
 
 # ----------------------------------------------------------------------------- CPU oracle arm
-def cpu_baseline(seconds: float = 15.0):
-    """The fp64 oracle, as it stands, on a bounded sample of the headline workload: all 64 heads of a set of
-    query tokens spread over the 32K sequence (SSA, (1,7,128)). Returns tokens/s of the oracle."""
+def cpu_baseline(seconds: float = 15.0, n: int = N_PREFILL):
+    """The fp64 oracle, as it stands, on a bounded sample of the headline workload: all 64 heads of random
+    query tokens of the n-token SSA prefill ((1,7,128)). Per token the oracle derives the allowed keys from its
+    own mask (oracle.allowed_keys) and attends over exactly those rows (oracle.attend); only those two calls
+    are timed (the rows are regenerated from the counter-based generator outside the timer).
+    Returns tokens/s of the oracle."""
     import oracle
     from inputs import TID_K, TID_Q, Spec, gen_rows_f32
-    qs = Spec(seed=0, tensor_id=TID_Q, batch=1, n=N_PREFILL, heads=H, d=D_QK)
-    ks = Spec(seed=0, tensor_id=TID_K, batch=1, n=N_PREFILL, heads=1, d=D_QK)
-    kf = gen_rows_f32(ks, 0, N_PREFILL)
-    vf = np.ascontiguousarray(kf[:, :D_V])
+    qs = Spec(seed=0, tensor_id=TID_Q, batch=1, n=n, heads=H, d=D_QK)
+    ks = Spec(seed=0, tensor_id=TID_K, batch=1, n=n, heads=1, d=D_QK)
     rng = np.random.default_rng(0)
     done, t0 = 0, time.perf_counter()
     spent = 0.0
+    s, l, b = PATTERN
+    kf = gen_rows_f32(ks, 0, n) if n <= 65536 else None  # whole KV once when small (75 MB at 32K)
     while spent < seconds:
-        toks = np.sort(rng.integers(0, N_PREFILL, 8))
-        for t in toks:
-            qr = gen_rows_f32(qs, int(t) * H, H)
+        for t in np.sort(rng.integers(0, n, 8)):
+            t = int(t)
+            qr = gen_rows_f32(qs, t * H, H)
+            lo = max(0, (t // b - l + 1) * b)
+            if kf is None:  # the rows the window can touch: sink blocks and the local blocks
+                rows = np.concatenate([np.arange(min(s * b, lo)), np.arange(lo, t + 1)])
+                kw = np.concatenate([gen_rows_f32(ks, 0, min(s * b, lo)), gen_rows_f32(ks, lo, t + 1 - lo)])
             ta = time.perf_counter()
-            oracle.attention_rows(qr, np.full(H, int(t)), kf, vf, loza_scale(), *PATTERN)
+            keys = oracle.allowed_keys(t, n, s, l, b)
+            kk = kf[keys] if kf is not None else kw[np.searchsorted(rows, keys)]
+            oracle.attend(qr, kk, kk[:, :D_V], loza_scale())
             spent += time.perf_counter() - ta
             done += 1
     wall = time.perf_counter() - t0
     return {"value": done / spent, "unit": "tokens/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{done} random query tokens x 64 heads of the 32K SSA prefill (fp64, OpenMP over rows); "
-                      f"{spent:.1f} s of oracle time ({wall:.1f} s wall incl. input regeneration)",
-            "cpu_model": _cpu_model()}
+            "sample": f"{done} random query tokens x 64 heads of the {n}-token SSA prefill (fp64, OpenMP over "
+                      f"rows; oracle.allowed_keys + oracle.attend per token); {spent:.1f} s of oracle time "
+                      f"({wall:.1f} s wall incl. input regeneration)",
+            "oracle_s": spent, "wall_s": wall, "cpu_model": _cpu_model()}
 
 
 def oracle_row_timings(seconds_each: float = 1.5):
@@ -681,30 +774,60 @@ def _cpu_model():
 
 
 def run_reference(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    """--impl reference: the fp64 oracle as it stands, on the host cores, on the GPU arm's config and metric
+    (N=1: the 32K prefill; N>1: the 1M-token sequence-parallel prefill). Each step is a bounded sample of that
+    workload; value = sampled tokens / oracle seconds. ms_per_step is the wall time a step actually took;
+    projected_full_step_ms is the oracle's time for the whole step at the sampled rate (a projection)."""
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    per = []
+    n_total = N_PREFILL if world == 1 else N_SP
+    per, walls = [], []
     cb = None
     for _ in range(args.warmup):
-        cpu_baseline(min(2.0, args.cpu_seconds))
+        cpu_baseline(min(2.0, args.cpu_seconds), n_total)
     for _ in range(args.steps):
-        cb = cpu_baseline(args.cpu_seconds / max(1, args.steps) * 2)
+        t0 = time.perf_counter()
+        cb = cpu_baseline(args.cpu_seconds / max(1, args.steps) * 2, n_total)
+        walls.append(time.perf_counter() - t0)
         per.append(cb["value"])
     value = float(np.mean(per))
     line = {"impl": "reference",
-            "metric": "SSA prefill tokens/s (B1 H64 n32768 MLA 576/512, (s,l,b)=(1,7,128)); % tensor roofline",
+            "metric": metric_name(world),
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": N_PREFILL / value * 1e3,  # one full 32K step at the sampled rate
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": float(np.mean(walls)) * 1e3,  # measured: one bounded sample per step
+            "projected_full_step_ms": n_total / value * 1e3,  # projection: the whole step at the sampled rate
+            "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (counter-based, seed 0)",
-            "config": {"workload": "ssa_prefill_32k", "batch": 1, "seq_len": N_PREFILL, "heads": H,
-                       "pattern": list(PATTERN)},
+            "config": {"workload": "ssa_prefill_32k" if world == 1 else "ssa_seqpar_prefill_1m", "batch": 1,
+                       "seq_len": n_total, "heads": H, "pattern": list(PATTERN)},
             "cpu_baseline": {"kind": "oracle", "cores": cb["cores"], "sample": cb["sample"], "value": value,
                              "unit": "tokens/s"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _relaunch_distributed(n):
+    """`bench.py --gpus N` without WORLD_SIZE: re-run this command under torch.distributed.run, one process per
+    GPU (NCCL_DEBUG=INFO so the rank count of the communicator is in the log). Fails loudly when the node has
+    fewer than N GPUs -- never a silent 1-GPU run."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        sys.stderr.write(f"bench.py: --gpus {n} needs {n} visible GPUs, this node has {have}\n")
+        sys.exit(2)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def main():
@@ -717,11 +840,20 @@ def main():
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-1m", action="store_true", help="skip the 1M-token single-GPU prefill row")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is not None and int(ws_env) != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={ws_env} but --gpus {args.gpus}\n")
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and ws_env is None:
+        _relaunch_distributed(args.gpus)
     else:
         run_gpu(args)
 
