@@ -90,12 +90,17 @@ loza_status_t ssa_prefill(const loza_attn_args_t* args, loza_pattern_t pattern, 
  * p = seq_lens[b] - 1 (seq_len INCLUDES the current token, DESIGN R8): reads only
  * the sink block(s) and the last l blocks of the cache, so its cost is
  * independent of the context length. args->n_q must be 1; args->n_kv = cache
- * capacity T_cap; seq_lens_dev [B] int32 on the device, 1 <= seq_len <= T_cap
- * (out-of-range values are clamped on the device). q [B,1,H,d_qk] -> o [B,1,H,d_v].
- * ws: loza_workspace_size(LOZA_WS_DECODE, ...) bytes, ZERO-FILLED before its first use (it holds
- * per-sequence split counters that every call leaves at zero again); bf16 path: H == 64. Kernel: a CTA
- * pair per sequence while 2*batch <= SM count (pair-cooperative by default; the environment variable
- * LOZA_DECODE_KERNEL=pair selects the key-split pair kernel), else a flattened split-KV kernel. */
+ * capacity T_cap; seq_lens_dev [B] int32 on the device, 1 <= seq_len <= T_cap. q [B,1,H,d_qk] ->
+ * o [B,1,H,d_v].
+ * ws: loza_workspace_size(LOZA_WS_DECODE, ...) bytes, initialised ONCE with loza_workspace_init (or any zero
+ * fill) before its first use; every call leaves it reusable. Bytes [0, 4) are an int32 status word: the
+ * kernels set it to LOZA_ERR_SHAPE when a seq_len was outside [1, T_cap] (they clamp it and continue); the
+ * caller reads and resets it. The rest holds the flattened kernel's per-sequence counters (left at zero by
+ * every call) and split partials.
+ * bf16 path kernels: while 2*batch <= SM count, a CTA pair per sequence -- the pair-cooperative kernel for
+ * H == 64 (attn_tc_decode_coop.cu), the key-split pair kernel for H < 64 (decode sharded by heads: every GPU
+ * still reads the whole latent window; attn_tc_decode_ks.cu); otherwise (H == 64 only) a flattened split-KV
+ * kernel. */
 loza_status_t ssa_decode(const loza_attn_args_t* args, const int32_t* seq_lens_dev,
                          loza_pattern_t pattern, void* ws, size_t ws_bytes, loza_stream_t stream);
 
@@ -189,8 +194,8 @@ loza_status_t ssa_ring_append(const void* rows, int64_t rows_stride_b, int64_t r
 /* ssa_decode over the bounded ring cache: args->k / args->v point into the ring cache, args->n_kv must be
  * (s+l)*b; seq_lens_dev are absolute lengths (any value >= 1: the ring holds the window of position
  * seq_len - 1 once positions [0, seq_len) were appended). Bitwise identical to ssa_decode over a contiguous
- * cache with the same rows. bf16, 64 heads, b % 128 == 0 and 2*batch <= SM count (the CTA-pair kernel);
- * else LOZA_ERR_UNSUPPORTED. No workspace. */
+ * cache with the same rows. bf16, H <= 64, b % 128 == 0 and 2*batch <= SM count (the CTA-pair kernels);
+ * else LOZA_ERR_UNSUPPORTED. No workspace (no status word: out-of-range seq_lens are clamped silently). */
 loza_status_t ssa_decode_ring(const loza_attn_args_t* args, const int32_t* seq_lens_dev, loza_pattern_t pattern,
                               loza_stream_t stream);
 
@@ -275,11 +280,21 @@ loza_status_t ssa_select_blocks(int64_t n_q, int64_t q_start, loza_pattern_t pat
 enum { LOZA_WS_DECODE = 0, LOZA_WS_FULL_DECODE = 1, LOZA_WS_BLEND = 2, LOZA_WS_SEQPAR = 3, LOZA_WS_BACKWARD = 4 };
 /* Workspace bytes for `which`; args may be NULL for LOZA_WS_BLEND. */
 size_t loza_workspace_size(int32_t which, const loza_attn_args_t* args, loza_pattern_t pattern, int32_t world);
+/* Zero-fill a workspace of `which` (its loza_workspace_size bytes) on `stream`: the required one-time
+ * initialisation of the decode workspaces (status word, split counters); harmless for the others. */
+loza_status_t loza_workspace_init(int32_t which, const loza_attn_args_t* args, loza_pattern_t pattern, int32_t world,
+                                  void* ws, size_t ws_bytes, loza_stream_t stream);
 
 const char* loza_status_string(loza_status_t status);
 const char* loza_last_error(void);           /* thread-local text of the last error, "" if none */
 uint64_t loza_kernel_launches(void);         /* number of library kernel launches so far (process) */
 int32_t loza_num_sms(void);                  /* SM count of the current device (0 if unknown) */
+/* Test hook: override the automatic kernel choice of a family, process-wide (the library never reads the
+ * environment). "decode": 0 auto, 1 pair-cooperative (H == 64), 2 key-split pair; "backward": 0 auto, 1 FFMA
+ * kernels, 2 warp-MMA key and row kernels, 3 tcgen05 key kernel + warp-MMA row kernel for dQ. A forced
+ * kernel that cannot take a problem falls back to the automatic choice. Returns 0, or -1 for an unknown
+ * family / variant. */
+int32_t loza_debug_force_kernel(const char* family, int32_t variant);
 
 #ifdef __cplusplus
 }

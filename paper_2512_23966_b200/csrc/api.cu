@@ -16,6 +16,9 @@ static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+static std::atomic<int> g_knobs[kNumKnobs];
+int knob(KnobFamily f) { return g_knobs[f].load(std::memory_order_relaxed); }
+
 int device_sm_count() {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;
@@ -109,7 +112,10 @@ loza_status_t choose_path(const loza_attn_args_t* a, const AttnProblem& p, Path*
     if (((int64_t)a->heads * a->n_q) % 128 != 0 && a->heads % 64 != 0)
       return fail(LOZA_ERR_UNSUPPORTED, "bf16 prefill needs H %% 64 == 0 or n_q*H %% 128 == 0");
   } else {
-    if (a->heads != 64) return fail(LOZA_ERR_UNSUPPORTED, "bf16 decode supports H == 64");
+    // H < 64 (decode sharded by heads) runs on the key-split pair kernel, whose Q rows >= H are zero-filled
+    if (a->heads > 64 || (a->heads != 64 && !decode_ks_eligible(p, device_sm_count())))
+      return fail(LOZA_ERR_UNSUPPORTED, "bf16 decode supports H == 64, or H < 64 on the SSA pair kernel "
+                                        "(2 * batch <= SMs, v aliasing k)");
     if (a->batch > 1024) return fail(LOZA_ERR_UNSUPPORTED, "bf16 decode supports batch <= 1024");
   }
   *path = Path::kTc;
@@ -295,10 +301,11 @@ loza_status_t ssa_decode_ring(const loza_attn_args_t* args, const int32_t* seq_l
   Path path;
   rc = choose_path(args, p, &path);
   if (rc != LOZA_OK) return rc;
-  if (path != Path::kTc || !decode_pair_eligible(p, device_sm_count()))
-    return fail(LOZA_ERR_UNSUPPORTED, "ring decode: bf16, H == 64, b %% 128 == 0, 2*batch <= SMs");
   p.ring = 1;
-  return cuda_status(launch_decode_pair_any(p, (cudaStream_t)stream), "decode_pair (ring) launch");
+  cudaError_t e;
+  if (path != Path::kTc || !decode_pair_dispatch(p, nullptr, (cudaStream_t)stream, &e))
+    return fail(LOZA_ERR_UNSUPPORTED, "ring decode: bf16, H <= 64, b %% 128 == 0, 2*batch <= SMs, v aliasing k");
+  return cuda_status(e, "decode (ring) launch");
 }
 
 loza_status_t ssa_select_blocks(int64_t n_q, int64_t q_start, loza_pattern_t pat, int32_t causal, int32_t* idx_dev,
@@ -336,6 +343,15 @@ size_t loza_workspace_size(int32_t which, const loza_attn_args_t* a, loza_patter
   return 0;
 }
 
+loza_status_t loza_workspace_init(int32_t which, const loza_attn_args_t* a, loza_pattern_t pat, int32_t world,
+                                  void* ws, size_t ws_bytes, loza_stream_t stream) {
+  g_last_error[0] = 0;
+  const size_t need = loza_workspace_size(which, a, pat, world);
+  if (need == 0) return LOZA_OK;
+  if (!ws || ws_bytes < need) return fail(LOZA_ERR_INVALID, "workspace too small (%zu < %zu)", ws_bytes, need);
+  return cuda_status(cudaMemsetAsync(ws, 0, need, (cudaStream_t)stream), "workspace init");
+}
+
 const char* loza_status_string(loza_status_t s) {
   switch (s) {
     case LOZA_OK: return "LOZA_OK";
@@ -350,6 +366,19 @@ const char* loza_status_string(loza_status_t s) {
 
 const char* loza_last_error(void) { return g_last_error; }
 uint64_t loza_kernel_launches(void) { return g_launches.load(); }
+
+int32_t loza_debug_force_kernel(const char* family, int32_t variant) {
+  if (!family) return -1;
+  if (strcmp(family, "decode") == 0 && variant >= 0 && variant <= 2) {
+    g_knobs[kKnobDecode].store(variant);
+    return 0;
+  }
+  if (strcmp(family, "backward") == 0 && variant >= 0 && variant <= 3) {
+    g_knobs[kKnobBackward].store(variant);
+    return 0;
+  }
+  return -1;
+}
 int32_t loza_num_sms(void) {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;

@@ -688,17 +688,11 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
   if (use_part && !part) return cudaErrorInvalidValue;
   const int64_t rows = (int64_t)a.n_q * a.heads;
   cudaError_t e;
-  // Key side: tcgen05 (attn_bwd_tc.cu) for the packed row layout (LOZA_BWD_KEYS=mma forces this file's key
+  // Key side: tcgen05 (attn_bwd_tc.cu) for the packed row layout (test knob backward = 2 forces this file's key
   // kernel). SSA: the tcgen05 key kernel also writes dS rows and dQ = dS K runs as a tcgen05 GEMM
-  // (LOZA_BWD_DQ=mma keeps this file's row kernel, which recomputes S and dP).
-  static const bool force_mma = [] {
-    const char* ev = getenv("LOZA_BWD_KEYS");
-    return ev && strcmp(ev, "mma") == 0;
-  }();
-  static const bool force_dq_mma = [] {
-    const char* ev = getenv("LOZA_BWD_DQ");
-    return ev && strcmp(ev, "mma") == 0;
-  }();
+  // (knob backward = 3 keeps this file's row kernel, which recomputes S and dP).
+  const bool force_mma = knob(kKnobBackward) == 2;
+  const bool force_dq_mma = knob(kKnobBackward) == 3;
   const bool tc_keys = !force_mma && backward_tc_eligible(a, dout);
   if (tc_keys && !force_dq_mma && ds && backward_ds_eligible(a) && rows > 0 && a.n_kv > 0) {
     if ((e = launch_bwd_D(a, dout, D, st)) != cudaSuccess) return e;

@@ -631,20 +631,25 @@ static size_t d_bytes(const AttnProblem& a) {
 }
 static size_t part_bytes(const AttnProblem& a) { return (backward_mma_part_bytes(a) + 255) / 256 * 256; }
 // D, then (tensor-core path, SSA) the sink-tile partials and the dS rows (attn_bwd_mma.cu / attn_bwd_tc.cu)
-size_t backward_ws_bytes(const AttnProblem& a) { return d_bytes(a) + part_bytes(a) + backward_ds_bytes(a); }
+// (the dS rows only when the tcgen05 dS path can run: bf16 MLA shape, V aliasing K, packed rows)
+size_t backward_ws_bytes(const AttnProblem& a) {
+  const auto& kv = a.kv.seg[0];
+  const bool v_alias = kv.v == kv.k && kv.v_st == kv.k_st && kv.v_sb == kv.k_sb;
+  const bool ds_path = a.in_bf16 && a.out_bf16 && a.d_qk == 576 && a.d_v == 512 && v_alias &&
+                       backward_tc_eligible(a, nullptr) && backward_ds_eligible(a);
+  return d_bytes(a) + part_bytes(a) + (ds_path ? backward_ds_bytes(a) : 0);
+}
 
 cudaError_t launch_attn_backward(const AttnProblem& a, const void* dout, float* dq, float* dk, float* dv, void* ws,
                                  cudaStream_t st) {
   if (a.d_qk > 32 * kMaxCQ || a.d_v > 32 * kMaxCV) return cudaErrorNotSupported;
-  // the absorbed MLA shape in bf16 runs on the tensor cores (LOZA_BWD_KERNEL=simt forces the FFMA kernels)
-  static const bool force_simt = [] {
-    const char* e = getenv("LOZA_BWD_KERNEL");
-    return e && strcmp(e, "simt") == 0;
-  }();
-  if (!force_simt && backward_mma_eligible(a, dout))
+  // the absorbed MLA shape in bf16 runs on the tensor cores (test knob backward = 1 forces the FFMA kernels)
+  if (knob(kKnobBackward) != 1 && backward_mma_eligible(a, dout))
     return launch_attn_backward_mma(
         a, dout, dq, dk, dv, reinterpret_cast<float*>(ws), reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + d_bytes(a)),
-        backward_ds_bytes(a) ? reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(ws) + d_bytes(a) + part_bytes(a)) : nullptr,
+        backward_ws_bytes(a) > d_bytes(a) + part_bytes(a)
+            ? reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(ws) + d_bytes(a) + part_bytes(a))
+            : nullptr,
         st);
   BwdParams p;
   p.q = a.q;

@@ -80,6 +80,7 @@ struct DecodeParams {
   float* lse;
   float* part;
   int32_t* counters;
+  int32_t* status;            // LOZA_ERR_SHAPE when a seq_len was outside [1, t_cap] (clamped)
   unsigned long long* trace;  // debug timeline of CTA 0 (NULL in production)
 };
 
@@ -90,6 +91,7 @@ struct SeqTiles {
 
 __device__ __forceinline__ SeqTiles seq_tiles(const DecodeParams& p, int bi) {
   int64_t L = p.seq_lens[bi];
+  if ((L < 1 || L > p.t_cap) && p.status) *p.status = LOZA_ERR_SHAPE;
   L = L < 1 ? 1 : (L > p.t_cap ? p.t_cap : L);
   SeqTiles t;
   t.pos = (int32_t)(L - 1);
@@ -601,16 +603,22 @@ int64_t decode_grid(const AttnProblem& a, int sms) {
 
 }  // namespace
 
+// decode workspace: [0, 256) status word (int32 at 0) + reserved, then (flattened kernel only) the per-sequence
+// counters and the split partials
 size_t decode_tc_ws_bytes(const AttnProblem& a) {
-  const int64_t G = decode_grid(a, device_sm_count());
-  return kCounterBytes + (size_t)(G + a.batch) * kPartBytes;
+  const int sms = device_sm_count();
+  if (decode_coop_eligible(a, sms) || decode_ks_eligible(a, sms)) return kDecodeStatusBytes;
+  const int64_t G = decode_grid(a, sms);
+  return kDecodeStatusBytes + kCounterBytes + (size_t)(G + a.batch) * kPartBytes;
 }
 
 unsigned long long* g_decode_trace = nullptr;
 
 cudaError_t launch_decode_tc(const AttnProblem& a, void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (decode_pair_eligible(a, device_sm_count())) return launch_decode_pair_any(a, st);
-  if (a.ring) return cudaErrorNotSupported;  // the ring cache is read by the pair kernel only
+  int32_t* status = ws && ws_bytes >= kDecodeStatusBytes ? reinterpret_cast<int32_t*>(ws) : nullptr;
+  cudaError_t pe;
+  if (decode_pair_dispatch(a, status, st, &pe)) return pe;
+  if (a.ring) return cudaErrorNotSupported;  // the ring cache is read by the key-split pair kernel only
   if (a.heads != kH) return cudaErrorNotSupported;
   if (a.batch > kMaxBatch) return cudaErrorNotSupported;
   if (a.n_kv >= (1ll << 31)) return cudaErrorNotSupported;
@@ -632,19 +640,17 @@ cudaError_t launch_decode_tc(const AttnProblem& a, void* ws, size_t ws_bytes, cu
   p.trace = g_decode_trace;
   const int sms = device_sm_count();
   p.grid = (int32_t)decode_grid(a, sms);
-  if (ws_bytes < kCounterBytes + (size_t)(p.grid + a.batch) * kPartBytes) return cudaErrorInvalidValue;
-  p.counters = reinterpret_cast<int32_t*>(ws);
-  p.part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kCounterBytes);
+  if (ws_bytes < kDecodeStatusBytes + kCounterBytes + (size_t)(p.grid + a.batch) * kPartBytes)
+    return cudaErrorInvalidValue;
+  p.status = status;
+  p.counters = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + kDecodeStatusBytes);
+  p.part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kDecodeStatusBytes + kCounterBytes);
   const KvSeg& s = a.kv.seg[0];
   if (!encode_3d(&p.q_map, a.q, kDqk, kH, a.batch, a.q_sh, a.q_sb, 64)) return cudaErrorInvalidValue;
   if (!encode_3d(&p.k_map, s.k, kDqk, (uint64_t)a.n_kv, a.batch, s.k_st, s.k_sb, 128)) return cudaErrorInvalidValue;
   if (!encode_3d(&p.v_map, s.v, kDv, (uint64_t)a.n_kv, a.batch, s.v_st, s.v_sb, 32)) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
+  if (e != cudaSuccess) return e;
   decode_tc_kernel<<<p.grid, kThreads, kSmemAlloc, st>>>(p);
   count_launch();
   return cudaGetLastError();

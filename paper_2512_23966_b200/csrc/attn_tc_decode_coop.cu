@@ -92,6 +92,7 @@ struct CoopParams {
   float* lse;
   unsigned long long* trace;  // debug timeline of cluster trace_cluster (NULL in production): [slot][rank][16]
   int32_t trace_cluster;
+  int32_t* status;  // nullable: LOZA_ERR_SHAPE when a seq_len was outside [1, t_cap] (clamped)
 };
 
 #define CTRACE(slot, idx)                                                                         \
@@ -280,6 +281,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
 
   const SeqTiles st = seq_tiles(p, bi);
   const int npt = (st.n_tiles + 1) / 2;  // pair tiles (>= 1)
+  if (p.status && threadIdx.x == 0 && cluster_ctarank() == 0) {
+    const int64_t L = p.seq_lens[bi];
+    if (L < 1 || L > p.t_cap) atomicExch(p.status, (int32_t)LOZA_ERR_SHAPE);
+  }
   CTRACE(0, 0);
 
   if (warp == 0) {
@@ -663,9 +668,30 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
 
 }  // namespace
 
-extern unsigned long long* g_pair_trace;  // attn_tc_decode_pair.cu (loza_debug_set_pair_trace)
+unsigned long long* g_pair_trace = nullptr;  // loza_debug_set_pair_trace
+int g_trace_cluster = 0;
 
-cudaError_t launch_decode_coop(const AttnProblem& a, cudaStream_t st) {
+bool decode_coop_eligible(const AttnProblem& a, int sms) {
+  return a.sparse && a.heads == kH && a.d_qk == kDqk && a.d_v == kDv && a.b % 128 == 0 &&
+         2 * (int64_t)a.batch <= sms && a.n_kv < (1ll << 31);
+}
+
+bool decode_pair_dispatch(const AttnProblem& a, int32_t* status, cudaStream_t st, cudaError_t* err) {
+  const int sms = device_sm_count();
+  const bool coop = decode_coop_eligible(a, sms), ks = decode_ks_eligible(a, sms);
+  const int k = knob(kKnobDecode);  // test override; a kernel that cannot take the problem is not forced
+  if (coop && k != 2) {
+    *err = launch_decode_coop(a, status, st);
+    return true;
+  }
+  if (ks) {
+    *err = launch_decode_ks(a, status, st);
+    return true;
+  }
+  return false;
+}
+
+cudaError_t launch_decode_coop(const AttnProblem& a, int32_t* status, cudaStream_t st) {
   if (a.heads != kH || a.d_qk != kDqk || a.d_v != kDv) return cudaErrorNotSupported;
   if (a.n_kv >= (1ll << 31)) return cudaErrorNotSupported;
   CoopParams p;
@@ -690,22 +716,17 @@ cudaError_t launch_decode_coop(const AttnProblem& a, cudaStream_t st) {
   p.out_bf16 = a.out_bf16;
   p.lse = a.lse;
   p.trace = g_pair_trace;
-  {
-    const char* e = getenv("LOZA_TRACE_CLUSTER");
-    p.trace_cluster = e ? atoi(e) : 0;
-  }
+  p.trace_cluster = g_trace_cluster;
+  p.status = status;
   const KvSeg& s = a.kv.seg[0];
   if (!encode_3d(&p.q_map, a.q, kDqk, kH, a.batch, a.q_sh, a.q_sb, 32)) return cudaErrorInvalidValue;
   if (!encode_3d(&p.k_map, s.k, kDqk, (uint64_t)a.n_kv, a.batch, s.k_st, s.k_sb, 128)) return cudaErrorInvalidValue;
   if (!encode_4d_chunks(&p.v_map, s.v, kDv, (uint64_t)a.n_kv, a.batch, s.v_st, s.v_sb, 32, 4))
     return cudaErrorInvalidValue;
   if (a.out_bf16 && !encode_3d(&p.o_map, a.o, kDv, kH, a.batch, a.o_sh, a.o_sb, 64)) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(decode_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  // per launch (the attribute is per device; a process may drive several GPUs)
+  cudaError_t ea = cudaFuncSetAttribute(decode_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
+  if (ea != cudaSuccess) return ea;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * a.batch));
   cfg.blockDim = dim3(kThreads);
@@ -723,3 +744,9 @@ cudaError_t launch_decode_coop(const AttnProblem& a, cudaStream_t st) {
 }
 
 }  // namespace loza
+
+// debug hooks (not part of include/loza.h): clock64 timeline of cluster `cluster` into dev_ptr
+extern "C" void loza_debug_set_pair_trace(void* dev_ptr, int32_t cluster) {
+  loza::g_pair_trace = (unsigned long long*)dev_ptr;
+  loza::g_trace_cluster = cluster;
+}

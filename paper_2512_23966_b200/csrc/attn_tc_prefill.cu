@@ -930,13 +930,12 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
     if (!encode_4d_chunks(&p.k2_map[i], s.k, kDqk, len, a.batch, s.k_st, s.k_sb, 128, 2)) return cudaErrorInvalidValue;
     if (!encode_4d_chunks(&p.v_map[i], s.v, kDv, len, a.batch, s.v_st, s.v_sb, kVKeys, 2)) return cudaErrorInvalidValue;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(prefill_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
+  {  // per launch (the attribute is per device; a process may drive several GPUs)
+    cudaError_t e = a.calib ? cudaFuncSetAttribute(prefill_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kSmemAlloc)
+                            : cudaFuncSetAttribute(prefill_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kSmemAlloc);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int sms = device_sm_count();
   int64_t ncl = sms / 2;

@@ -663,11 +663,9 @@ cudaError_t launch_prefill_mha(const AttnProblem& a, int64_t k_sh, int64_t v_sh,
     return cudaErrorInvalidValue;
   if (a.out_bf16 && !encode_5d_heads(&p.o_map, a.o, kDv, (uint64_t)a.n_q, H, a.batch, a.o_st, a.o_sh, a.o_sb, 128, 1))
     return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
+  {  // per launch (the attribute is per device; a process may drive several GPUs)
     cudaError_t e = cudaFuncSetAttribute(prefill_mha_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int sms = device_sm_count();
   int64_t ncl = sms / 2;

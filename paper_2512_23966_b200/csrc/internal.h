@@ -67,13 +67,20 @@ cudaError_t launch_dalpha_reduce(const double* part, int n, const float* alpha, 
 cudaError_t launch_prefill_tc(const AttnProblem& p, cudaStream_t st);
 // non-absorbed (MHA) form, d_qk 192 / d_v 128, per-head K/V (k_sh, v_sh: head strides in elements)
 // pair-cooperative SSA decode (attn_tc_decode_coop.cu): same eligibility as the pair kernel
-cudaError_t launch_decode_coop(const AttnProblem& a, cudaStream_t st);
-cudaError_t launch_decode_pair_any(const AttnProblem& a, cudaStream_t st);
+cudaError_t launch_decode_coop(const AttnProblem& a, int32_t* status, cudaStream_t st);
+// pair-cooperative eligibility: SSA, H == 64, b % 128 == 0, 2 * batch <= SMs
+bool decode_coop_eligible(const AttnProblem& a, int sms);
+// the SSA decode kernel for a problem the CTA-pair kernels take (coop for H == 64, key-split for H < 64; the
+// decode test knob overrides); false if neither is eligible
+bool decode_pair_dispatch(const AttnProblem& a, int32_t* status, cudaStream_t st, cudaError_t* err);
 cudaError_t launch_prefill_mha(const AttnProblem& a, int64_t k_sh, int64_t v_sh, cudaStream_t st);
 cudaError_t launch_decode_tc(const AttnProblem& p, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t decode_tc_ws_bytes(const AttnProblem& p);
-bool decode_pair_eligible(const AttnProblem& a, int sms);
-cudaError_t launch_decode_pair(const AttnProblem& a, cudaStream_t st);
+// key-split pair SSA decode (attn_tc_decode_ks.cu): SSA, H <= 64, b % 128 == 0, V aliasing the KV rows,
+// 2 * batch <= SMs; status (nullable) receives LOZA_ERR_SHAPE when a seq_len is clamped
+constexpr size_t kDecodeStatusBytes = 256;
+bool decode_ks_eligible(const AttnProblem& a, int sms);
+cudaError_t launch_decode_ks(const AttnProblem& a, int32_t* status, cudaStream_t st);
 size_t backward_ws_bytes(const AttnProblem& a);
 // tensor-core backward (attn_bwd_mma.cu): bf16, d_qk 576, d_v 512, V = K[:, :512]; D [B][n_q*H] and the
 // sink-tile partials (backward_mma_part_bytes) come from the backward workspace
@@ -98,6 +105,11 @@ cudaError_t launch_ring_append(const void* rows, int64_t r_sb, int64_t r_st, int
                                int32_t batch, int32_t row_bytes, cudaStream_t st);
 
 void count_launch(uint64_t n = 1);
+// Test-only kernel overrides (loza_debug_force_kernel; never read from the environment): 0 = automatic choice.
+// decode: 1 = pair-cooperative (H == 64 only), 2 = key-split pair. backward: 1 = FFMA kernels, 2 = warp-MMA key and
+// row kernels, 3 = tcgen05 key kernel + warp-MMA row kernel for dQ.
+enum KnobFamily { kKnobDecode = 0, kKnobBackward = 1, kNumKnobs = 2 };
+int knob(KnobFamily f);
 loza_status_t fail(loza_status_t st, const char* fmt, ...);
 loza_status_t cuda_status(cudaError_t e, const char* what);
 loza_status_t make_problem(const loza_attn_args_t* a, bool sparse, loza_pattern_t pat, const int32_t* seq_lens,

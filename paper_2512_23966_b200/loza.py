@@ -27,7 +27,8 @@ EXPORTS = ["ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_pref
            "ssa_prefill_mha", "ssa_ring_append",
            "ssa_decode_ring", "ssa_seqpar_prefill", "loza_seqpar_plan", "loza_seqpar_segments",
            "loza_seqpar_prefill_local", "loza_seqpar_prefill_loopback", "ssa_select_blocks", "loza_workspace_size", "loza_status_string",
-           "loza_last_error", "loza_kernel_launches", "loza_num_sms"]
+           "loza_last_error", "loza_kernel_launches", "loza_num_sms", "loza_debug_force_kernel",
+           "loza_workspace_init"]
 
 
 class LozaError(RuntimeError):
@@ -97,6 +98,10 @@ def lib():
         L.loza_last_error.restype = ctypes.c_char_p
         L.loza_kernel_launches.restype = ctypes.c_uint64
         L.loza_num_sms.restype = I32
+        L.loza_debug_force_kernel.argtypes = [ctypes.c_char_p, I32]
+        L.loza_debug_force_kernel.restype = I32
+        L.loza_workspace_init.argtypes = [I32, P(AttnArgs), Pattern, I32, V, SZ, V]
+        L.loza_workspace_init.restype = S
         for fn in ("ssa_prefill", "ssa_decode", "full_attn_ref", "loza_blend", "ssa_seqpar_prefill",
                    "loza_seqpar_prefill_local", "loza_seqpar_prefill_loopback", "ssa_select_blocks"):
             getattr(L, fn).restype = S
@@ -111,6 +116,13 @@ def _check(rc: int):
 
 def kernel_launches() -> int:
     return int(lib().loza_kernel_launches())
+
+
+def force_kernel(family: str, variant: int) -> None:
+    """Test hook (loza_debug_force_kernel): family "decode" (0 auto, 1 pair-cooperative, 2 key-split pair) or
+    "backward" (0 auto, 1 FFMA, 2 warp-MMA keys and rows, 3 tcgen05 keys + warp-MMA dQ)."""
+    if lib().loza_debug_force_kernel(family.encode(), int(variant)) != 0:
+        raise ValueError(f"unknown kernel override {family}={variant}")
 
 
 def _dt(t: torch.Tensor) -> int:
@@ -209,11 +221,7 @@ def ssa_prefill_blend(q, k, o_full, alpha, d_o_hat=None, v=None, pattern=PAPER_P
     if d_o_hat is not None:
         assert d_o_hat.shape == o.shape and d_o_hat.dtype == torch.bfloat16 and d_o_hat.is_contiguous()
         d_alpha = torch.empty(1, dtype=torch.float64, device=q.device)
-    need = lib().loza_workspace_size(LOZA_WS_BLEND, None, Pattern(0, 1, 1), 1)
-    dev = q.device
-    ws = _blend_ws.get(dev)
-    if ws is None:
-        ws = _blend_ws[dev] = torch.empty(need, dtype=torch.uint8, device=dev)
+    need, ws = _blend_workspace(stream)
     V = ctypes.c_void_p
     _check(lib().ssa_prefill_blend(ctypes.byref(a), _pattern(pattern), V(o_full.data_ptr()), V(alpha.data_ptr()),
                                    V(d_o_hat.data_ptr() if d_o_hat is not None else 0),
@@ -244,7 +252,8 @@ def attention_backward(q, k, o, lse, d_o, v=None, pattern=PAPER_PATTERN, scale=N
     dvv = torch.empty((B, n_kv, dv), dtype=torch.float32, device=q.device)
     pat = pattern if pattern is not None else (0, 1, 1)
     need = lib().loza_workspace_size(LOZA_WS_BACKWARD, ctypes.byref(a), _pattern(pat), 1)
-    ws = torch.empty(max(need, 1), dtype=torch.uint8, device=q.device)
+    with torch.cuda.stream(torch.cuda.current_stream() if stream is None else stream):  # freed after the launch
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=q.device)
     V = ctypes.c_void_p
     _check(lib().attention_backward(ctypes.byref(a), 1 if pattern is not None else 0, _pattern(pat),
                                     V(do4.data_ptr()), V(dq.data_ptr()), V(dk.data_ptr()), V(dvv.data_ptr()),
@@ -315,19 +324,34 @@ def ssa_decode_ring(q, cache, seq_lens, v=None, pattern=PAPER_PATTERN, scale=Non
 _decode_ws_cache = {}
 
 
-def _decode_ws(which, a, pattern, ws):
-    """Decode workspace: split-KV partials + per-sequence counters. The counters must start at zero and the
-    kernel leaves them at zero, so a zero-filled buffer is allocated once per device and reused."""
+def _decode_ws(which, a, pattern, ws, stream):
+    """Decode workspace (include/loza.h): a status word, then (flattened split-KV kernel) per-sequence counters and
+    partials. It must start zeroed (loza_workspace_init) and every call leaves the counters at zero, so one buffer
+    is initialised once per (device, stream) and reused; concurrent streams get their own."""
     need = lib().loza_workspace_size(which, ctypes.byref(a), _pattern(pattern), 1)
     if need == 0:
         return None, 0
     if ws is None or ws.numel() < need:
-        dev = torch.cuda.current_device()
-        ws = _decode_ws_cache.get(dev)
+        s = torch.cuda.current_stream() if stream is None else stream
+        key = (s.device.index, s.cuda_stream, which)
+        ws = _decode_ws_cache.get(key)
         if ws is None or ws.numel() < need:
-            ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
-            _decode_ws_cache[dev] = ws
+            with torch.cuda.stream(s):
+                ws = torch.empty(need, dtype=torch.uint8, device=s.device)
+            _check(lib().loza_workspace_init(which, ctypes.byref(a), _pattern(pattern), 1,
+                                             ctypes.c_void_p(ws.data_ptr()), need, ctypes.c_void_p(s.cuda_stream)))
+            _decode_ws_cache[key] = ws
     return ws, need
+
+
+def decode_status(ws) -> int:
+    """The status word of a decode workspace: LOZA_ERR_SHAPE (2) once some seq_len was outside [1, n_kv] (the
+    kernels clamp it and continue), else 0. Synchronises with the device."""
+    return int(ws[:4].view(torch.int32).item())
+
+
+def decode_status_reset(ws, stream=None):
+    ws[:4].zero_()
 
 
 def ssa_decode(q, cache, seq_lens, v=None, pattern=PAPER_PATTERN, scale=None, *, d_v=512, out=None, lse=None,
@@ -341,7 +365,7 @@ def ssa_decode(q, cache, seq_lens, v=None, pattern=PAPER_PATTERN, scale=None, *,
     o4 = o if o.dim() == 4 else o.unsqueeze(1)
     a = make_args(q4, k, v, o4, scale=scale, lse=lse)
     assert seq_lens.dtype == torch.int32 and seq_lens.is_cuda
-    w, need = _decode_ws(LOZA_WS_DECODE, a, pattern, ws)
+    w, need = _decode_ws(LOZA_WS_DECODE, a, pattern, ws, stream)
     _check(lib().ssa_decode(ctypes.byref(a), ctypes.c_void_p(seq_lens.data_ptr()), _pattern(pattern),
                             ctypes.c_void_p(w.data_ptr() if w is not None else 0), need, _stream(stream)))
     return o if q.dim() == 4 else o4[:, 0]
@@ -362,13 +386,25 @@ def full_attn_ref(q, k, v=None, scale=None, *, seq_lens=None, causal=True, d_v=5
                                                 device=q4.device)
     o4 = o if o.dim() == 4 else o.unsqueeze(1)
     a = make_args(q4, k, v, o4, scale=scale, causal=causal, lse=lse)
-    w, need = _decode_ws(LOZA_WS_FULL_DECODE, a, (0, 1, 1), ws)
+    w, need = _decode_ws(LOZA_WS_FULL_DECODE, a, (0, 1, 1), ws, stream)
     _check(lib().full_attn_ref(ctypes.byref(a), ctypes.c_void_p(seq_lens.data_ptr()),
                                ctypes.c_void_p(w.data_ptr() if w is not None else 0), need, _stream(stream)))
     return o if q.dim() == 4 else o4[:, 0]
 
 
 _blend_ws = {}
+
+
+def _blend_workspace(stream):
+    """Per-CTA d_alpha partials (written and reduced inside one call): one buffer per (device, stream)."""
+    need = lib().loza_workspace_size(LOZA_WS_BLEND, None, Pattern(0, 1, 1), 1)
+    s = torch.cuda.current_stream() if stream is None else stream
+    key = (s.device.index, s.cuda_stream)
+    ws = _blend_ws.get(key)
+    if ws is None:
+        with torch.cuda.stream(s):
+            ws = _blend_ws[key] = torch.empty(need, dtype=torch.uint8, device=s.device)
+    return need, ws
 
 
 def loza_blend(o_full, o_sparse, alpha, d_o_hat=None, *, out=None, d_alpha=None, status=None, want_out=True,
@@ -385,10 +421,7 @@ def loza_blend(o_full, o_sparse, alpha, d_o_hat=None, *, out=None, d_alpha=None,
         assert d_o_hat.shape == o_full.shape and d_o_hat.dtype == o_full.dtype and d_o_hat.is_contiguous()
         if d_alpha is None:
             d_alpha = torch.empty(1, dtype=torch.float64, device=dev)
-    need = lib().loza_workspace_size(LOZA_WS_BLEND, None, Pattern(0, 1, 1), 1)
-    ws = _blend_ws.get(dev)
-    if ws is None:
-        ws = _blend_ws[dev] = torch.empty(need, dtype=torch.uint8, device=dev)
+    need, ws = _blend_workspace(stream)
     V = ctypes.c_void_p
     _check(lib().loza_blend(V(o_full.data_ptr()), V(o_sparse.data_ptr()), V(alpha.data_ptr()),
                             V(o_hat.data_ptr() if o_hat is not None else 0),
@@ -427,7 +460,8 @@ def ssa_seqpar_prefill(q_shard, k_shard, v=None, pattern=PAPER_PATTERN, scale=No
     a = make_args(q_shard, k_shard, v, o, scale=scale, q_start=rank * n_local, lse=lse)
     need = int(lib().loza_workspace_size(LOZA_WS_SEQPAR, ctypes.byref(a), _pattern(pattern), world))
     if ws is None or ws.numel() < need:
-        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=q_shard.device)
+        with torch.cuda.stream(torch.cuda.current_stream() if stream is None else stream):
+            ws = torch.empty(max(need, 1), dtype=torch.uint8, device=q_shard.device)
     _check(lib().ssa_seqpar_prefill(ctypes.byref(a), _pattern(pattern), ctypes.c_void_p(comm_ptr), rank, world,
                                     ctypes.c_void_p(ws.data_ptr()), need, _stream(stream)))
     return o
@@ -443,7 +477,8 @@ def ssa_seqpar_prefill_local(q_shard, k_shard, v=None, pattern=PAPER_PATTERN, sc
     o = out if out is not None else _alloc_out(q_shard, v.shape[-1], out_dtype)
     a = make_args(q_shard, k_shard, v, o, scale=scale, q_start=rank * n_local, lse=lse)
     need = int(lib().loza_workspace_size(LOZA_WS_SEQPAR, ctypes.byref(a), _pattern(pattern), world))
-    ws = torch.empty(max(need, 1), dtype=torch.uint8, device=q_shard.device)
+    with torch.cuda.stream(torch.cuda.current_stream() if stream is None else stream):
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=q_shard.device)
     V = ctypes.c_void_p
 
     def ptr(t):

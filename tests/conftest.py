@@ -11,6 +11,13 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running")
+    # test-only kernel overrides: the library never reads the environment; a test process that re-runs a parity
+    # suite through an alternative kernel sets these, and they are applied here through loza_debug_force_kernel
+    for family, var in (("decode", "LOZA_TEST_DECODE_KERNEL"), ("backward", "LOZA_TEST_BACKWARD_KERNEL")):
+        v = os.environ.get(var)
+        if v:
+            from paper_2512_23966_b200 import loza
+            loza.force_kernel(family, int(v))
 
 
 def pytest_collection_modifyitems(config, items):

@@ -187,23 +187,24 @@ def test_backward_mla_mma(sparse, causal, q0, H, n, pat, B, ofwd):
 
 
 def test_backward_mla_simt_forced():
-    """LOZA_BWD_KERNEL=simt keeps the FFMA kernels reachable for the MLA shape: the bf16 MLA test through them."""
+    """The FFMA kernels stay reachable for the MLA shape (test knob backward = 1, loza_debug_force_kernel, set by
+    tests/conftest.py from LOZA_TEST_BACKWARD_KERNEL): the bf16 MLA test through them."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(root, "tests", "test_gpu_backward.py") + "::test_backward_mla_bf16_ssa"],
-                       cwd=root, env=dict(os.environ, LOZA_BWD_KERNEL="simt"), capture_output=True, text=True,
+                       cwd=root, env=dict(os.environ, LOZA_TEST_BACKWARD_KERNEL="1"), capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("env", [{"LOZA_BWD_KEYS": "mma"}, {"LOZA_BWD_DQ": "mma"}])
+@pytest.mark.parametrize("env", [{"LOZA_TEST_BACKWARD_KERNEL": "2"}, {"LOZA_TEST_BACKWARD_KERNEL": "3"}])
 def test_backward_mma_paths_forced(env):
-    """The warp-level-MMA kernels of attn_bwd_mma.cu kept reachable through the MLA parity cases:
-    LOZA_BWD_KEYS=mma (its key kernel and row kernel instead of the tcgen05 key kernel and dS GEMM) and
-    LOZA_BWD_DQ=mma (tcgen05 key kernel, dQ by the row kernel instead of the tcgen05 dS GEMM)."""
+    """The warp-level-MMA kernels of attn_bwd_mma.cu kept reachable through the MLA parity cases (test knob
+    backward, loza_debug_force_kernel): 2 = its key kernel and row kernel instead of the tcgen05 key kernel and
+    dS GEMM; 3 = tcgen05 key kernel, dQ by the row kernel instead of the tcgen05 dS GEMM."""
     import os
     import subprocess
     import sys

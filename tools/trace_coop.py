@@ -11,7 +11,7 @@ q = empty_filled(Spec(seed=1, tensor_id=TID_Q, batch=B, n=1, heads=64, d=576))
 seq = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
 tr = torch.zeros(11 * 2 * 16 + 32 * B, dtype=torch.int64, device="cuda")
 L = loza.lib()
-L.loza_debug_set_pair_trace.argtypes = [ctypes.c_void_p]
+L.loza_debug_set_pair_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 for _ in range(3):
     loza.ssa_decode(q, cache, seq)
 torch.cuda.synchronize()
@@ -19,10 +19,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "cold":
     fl = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     fl.fill_(1)
     torch.cuda.synchronize()
-L.loza_debug_set_pair_trace(ctypes.c_void_p(tr.data_ptr()))
+L.loza_debug_set_pair_trace(ctypes.c_void_p(tr.data_ptr()), 0)
 loza.ssa_decode(q, cache, seq)
 torch.cuda.synchronize()
-L.loza_debug_set_pair_trace(ctypes.c_void_p(0))
+L.loza_debug_set_pair_trace(ctypes.c_void_p(0), 0)
 ta = tr.cpu().numpy().astype("int64")
 t = ta[:11 * 2 * 16].reshape(11, 2, 16)
 sp4 = ta[11 * 2 * 16:11 * 2 * 16 + 16 * B].reshape(2 * B, 8)
