@@ -259,6 +259,11 @@ def run_gpu(args):
     rows = {}
     if rank == 0 and world == 1 and not args.quick:
         rows = extra_rows(args, q, kv, o, flush, peaks)
+    if world > 1 and not args.quick and not args.no_decode:
+        try:
+            rows["decode_batch_sharded_128k"] = decode_sharded_leg(world, rank, dev, flush, peaks)
+        except Exception as ex:  # noqa: BLE001 -- reported in the line
+            rows["decode_batch_sharded_128k"] = {"error": repr(ex)[:300]}
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -573,6 +578,54 @@ def prefill_1m_row(peaks, flush, steps=5, warmup=2):
                        "l2": "inputs (146 GB) exceed L2; flushed between steps anyway"}}
 
 
+def time_decode_graph(q, cache, seqs, outs, flush, R=64):
+    """Per-step time (ms) of ssa_decode captured R times in one CUDA graph over rotating windows/outputs (a serving
+    engine graph-captures the decode step), L2 flushed before each replay; median of 5 replays."""
+    import torch
+
+    from paper_2512_23966_b200 import loza
+    scale = loza.default_scale(D_QK)
+    for r in range(len(seqs)):  # warm-up (also initialises the decode workspace outside the capture)
+        loza.ssa_decode(q, cache, seqs[r], pattern=PATTERN, scale=scale, out=outs[r])
+    torch.cuda.synchronize()
+    gs = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.stream(cs):
+        with torch.cuda.graph(gs, stream=cs):
+            for i in range(R):
+                loza.ssa_decode(q, cache, seqs[i % len(seqs)], pattern=PATTERN, scale=scale, out=outs[i % len(outs)])
+    torch.cuda.synchronize()
+    tg = _time_events(lambda: gs.replay(), 5, 2, flush)
+    return float(np.median(tg)) / R
+
+
+def decode_sharded_leg(world, rank, dev, flush, peaks):
+    """Decode sharded by batch at N > 1 (SURVEY.md §8 e; no collective): every rank decodes its own 64 sequences
+    at 128K context (weak scaling: 64 sequences per GPU); value = all ranks' sequences / max-rank step time."""
+    import torch
+    import torch.distributed as dist
+
+    from inputs import TID_K, TID_Q, Spec
+    from inputs.device import fill_
+    B, ctx = 64, 131072
+    cache = torch.empty((B, ctx, D_QK), dtype=torch.bfloat16, device=dev)
+    fill_(cache, Spec(seed=0, tensor_id=TID_K, batch=B * world, n=ctx, heads=1, d=D_QK), row_start=rank * B * ctx)
+    q = torch.empty((B, 1, H, D_QK), dtype=torch.bfloat16, device=dev)
+    fill_(q, Spec(seed=1, tensor_id=TID_Q, batch=B * world, n=1, heads=H, d=D_QK), row_start=rank * B * H)
+    seqs = [torch.full((B,), ctx - 2048 * r, dtype=torch.int32, device=dev) for r in range(4)]
+    outs = [torch.empty((B, 1, H, D_V), dtype=torch.bfloat16, device=dev) for _ in range(4)]
+    ms = time_decode_graph(q, cache, seqs, outs, flush)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    by = world * B * (1024 * D_QK * 2 + H * D_QK * 2 + H * D_V * 2)
+    del cache
+    return {"ssa_us_per_step": ms * 1e3, "sequences_per_gpu": B, "context": ctx,
+            "tokens_per_s": world * B / (ms * 1e-3), "gbs_all_ranks": by / (ms * 1e-3) / 1e9,
+            "frac_hbm_per_gpu": by / world / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], "scaling": "weak",
+            "timing": "CUDA graph of 64 steps, 4 rotating windows, max over ranks"}
+
+
 def decode_rows(args, peaks, flush):
     import torch
 
@@ -633,24 +686,28 @@ def decode_rows(args, peaks, flush):
         # is not timed (a serving engine graph-captures the decode step).
         seqs = [torch.full((B,), ctx - 2048 * r, dtype=torch.int32, device=dev) for r in range(4)]
         outs = [torch.empty((B, 1, H, D_V), dtype=torch.bfloat16, device=dev) for _ in range(4)]
-        for r in range(4):  # warm-up (also allocates the decode workspace outside the capture)
-            loza.ssa_decode(qd, cache, seqs[r], pattern=PATTERN, scale=scale, out=outs[r])
-        torch.cuda.synchronize()
         R = 64
-        gs = torch.cuda.CUDAGraph()
-        cs = torch.cuda.Stream()
-        with torch.cuda.stream(cs):
-            with torch.cuda.graph(gs, stream=cs):
-                for i in range(R):
-                    loza.ssa_decode(qd, cache, seqs[i % 4], pattern=PATTERN, scale=scale, out=outs[i % 4])
-        torch.cuda.synchronize()
-        tg = _time_events(lambda: gs.replay(), 5, 2, flush)
-        ms = float(np.median(tg)) / R
+        ms = time_decode_graph(qd, cache, seqs, outs, flush, R)
         window = min(ctx, (PATTERN[0] + PATTERN[1]) * PATTERN[2])
         by = B * (window * D_QK * 2 + H * D_QK * 2 + H * D_V * 2)
         res[str(ctx)] = {"ssa_us": ms * 1e3, "ssa_tokens_per_s": B / (ms * 1e-3), "ssa_gbs": by / (ms * 1e-3) / 1e9,
                          "ssa_frac_hbm": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                          "ssa_bytes": by, "ssa_timing": f"CUDA graph of {R} steps, 4 rotating windows"}
+    # decode sharded by heads (north star; SURVEY.md §8 e "if B < R"): one GPU's share of a head-sharded decode,
+    # B64 with H/2 = 32 heads over the same latent windows (the key-split pair kernel, attn_tc_decode_ks.cu);
+    # per-GPU bytes hardly drop (the window is shared by all heads)
+    if "131072" in res:
+        ctx, Hs = 131072, 32
+        qh = qd[:, :, :Hs].contiguous()
+        seqs = [torch.full((B,), ctx - 2048 * r, dtype=torch.int32, device=dev) for r in range(4)]
+        outs = [torch.empty((B, 1, Hs, D_V), dtype=torch.bfloat16, device=dev) for _ in range(4)]
+        ms = time_decode_graph(qh, cache, seqs, outs, flush)
+        by = B * (1024 * D_QK * 2 + Hs * D_QK * 2 + Hs * D_V * 2)
+        res["heads32_131072"] = {"ssa_us": ms * 1e3, "ssa_tokens_per_s": B / (ms * 1e-3),
+                                 "ssa_gbs": by / (ms * 1e-3) / 1e9,
+                                 "ssa_frac_hbm": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                 "kernel": "key-split pair (attn_tc_decode_ks.cu)",
+                                 "note": "B64, 32 of 64 heads: one GPU of a 2-way head-sharded decode"}
     # full-attention comparators after every SSA row (their long max-bandwidth runs heat the GPU and slowed
     # SSA rows timed right after them by up to 30%)
     for ctx in (131072, 524288, 1048576):
