@@ -7,12 +7,16 @@
 //    (M256 N64: 43 cycles for the pair vs 2 x 48 for two M128 N64 streams).
 //  * Softmax per CTA over its own keys with a SHARED running max per head: each CTA reduces its per-head tile
 //    maximum and swaps the 64 values with the partner through DSMEM, so both CTAs use the same max and
-//    their P values can enter one MMA. A thread (key k, heads 32 ch ..) writes its 32 P values (64 B) into
-//    the P buffer of CTA ch (local, or DSMEM for the partner's heads): P_r = [256 keys][32 heads] bf16,
-//    SWIZZLE_64B MN-major (the B operand half of CTA r).
+//    their P values can enter one MMA; lane j of a warp takes the lazy-rescale decision for head j and the
+//    warp reads the 32 (m, corr) pairs back as smem broadcasts. A thread (key k, heads 32 ch ..) writes its
+//    32 P values (64 B): own heads into this CTA's P half, the partner's heads into a staging block that the
+//    transfer warp moves with ONE 8 KB bulk DSMEM copy (completion on the receiver's barrier, spin-waited);
+//    P_r = [256 keys][32 heads] bf16, SWIZZLE_64B MN-major (the B operand half of CTA r).
 //  * O^T += V^T P: 32 UMMAs M256 (dims: CTA r owns dims [256 r, 256 r + 256), two 128-dim groups) N64
 //    (heads) K16 over all 256 keys; each CTA streams V rows of both sub-blocks for its 256 dims. The per-head
-//    sums l are swapped once at the end; each CTA normalises and stores its own dims (no O exchange).
+//    sums l are swapped once at the end through an mbarrier (the other roles do not wait); each CTA
+//    normalises its own dims and stores them straight from registers (lane pairs swap one value per head pair
+//    so every store is a bf16x2); the final cluster barrier is relaxed (no wait for the stores to drain).
 //  * Loads: warp 0 of each CTA (Q halves first through 9 chunk barriers; then a ring of 4 x 32 KB items in
 //    MMA order K(0), K(1), V(0), K(2), V(1), ...; pair TMA with completion on the leader's barriers);
 //    warp 1 of the leader issues every UMMA; warps 2-9 of both CTAs run the softmax.
@@ -55,18 +59,18 @@ constexpr int kBarPFull = kBarSFree + 2;          // [2]
 constexpr int kBarOFull = kBarPFull + 2;          // [2]
 constexpr int kBarMax = kBarOFull + 2;            // [2] partner's tile maxima landed (bulk copy, local)
 constexpr int kBarPStaged = kBarMax + 2;          // [2] the partner's-heads P rows are staged (4 warps, local)
-constexpr int kBarL = kBarPStaged + 2;              // partner's sums landed (local)
+constexpr int kBarPRecv = kBarPStaged + 2;         // [2] the partner's P rows landed here (bulk copy, local)
+constexpr int kBarL = kBarPRecv + 2;              // partner's sums landed (local)
 constexpr int kNumBars = kBarL + 1;
 constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
 constexpr int kOffRed = (kOffTmemPtr + 4 + 15) & ~15;  // float [2 buf][4 key quarters][64 heads]
 constexpr int kOffX = kOffRed + 2 * 4 * 64 * 4;       // float partner maxima [2 buf][64], partner sums [64]
 constexpr int kOffXl = kOffX + 3 * 64 * 4;            // float own maxima [2 buf][64], own sums [64] (copy sources)
 constexpr int kOffInv = kOffXl + 3 * 64 * 4;          // float 1/l [64]
-constexpr int kSmemUsed = kOffInv + 64 * 4;
+constexpr int kOffHm = kOffInv + 64 * 4;             // float per softmax warp: -m [32], corr [32]
+constexpr int kSmemUsed = kOffHm + 8 * 64 * 4;
 constexpr int kSmemAlloc = kSmemUsed;
 static_assert(kSmemAlloc <= 232448, "smem");
-constexpr int kOffOut = kOffP;  // bf16 output staging [4 boxes][64 heads][64 dims] in the idle P buffers
-static_assert(4 * 8192 <= 2 * kPBytes, "output staging fits the P buffers");
 
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kTmemO = 0, kTmemS = 128;  // O^T group g at 64 g (lanes = dims), S^T buffer b at 128 + 64 b
@@ -76,7 +80,7 @@ constexpr uint32_t kArrivalsPerPair = 2 * kSoftmaxWarps;
 constexpr uint32_t kPFullArrivals = kArrivalsPerPair + 2;  // + the transfer warp of each CTA
 
 struct CoopParams {
-  CUtensorMap q_map, k_map, v_map, o_map;
+  CUtensorMap q_map, k_map, v_map;
   const int32_t* seq_lens;
   int32_t batch, s, l, b;
   int32_t ring;
@@ -137,12 +141,6 @@ __device__ __forceinline__ int32_t kv_row(const CoopParams& p, int32_t k0) {
   if (kb < p.s) return k0;
   return p.s * p.b + ((kb - p.s) % p.l) * p.b + (k0 - kb * p.b);
 }
-__device__ __forceinline__ float m_used_lane(const float (&m)[32], uint32_t lane) {
-  float r = m[0];
-#pragma unroll
-  for (int j = 1; j < 32; ++j) r = (j == (int)lane) ? m[j] : r;
-  return r;
-}
 // smem descriptor, SWIZZLE_64B (layout type 4), version 1
 __device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   uint64_t d = 0;
@@ -153,7 +151,6 @@ __device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr, uint32_t lbo_byte
   d |= (uint64_t)4 << 61;
   return d;
 }
-__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 // cluster-scope release arrive / acquire wait: used only where generic-proxy data crosses CTAs (the swapped
 // maxima and sums, the partner's P rows) -- the default .cta semantics elsewhere (see sm100.cuh)
 __device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cbar) {
@@ -187,9 +184,6 @@ __device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
 }
 __device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_cluster() {
-  asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
 }
 
 #define FULL_L(slot) (full_l + 8 * (slot))
@@ -236,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       mbar_init(bar(kBarOFull + i), 1);
       mbar_init(bar(kBarMax + i), 1);    // armed each tile (expect_tx 256 B), completed by the partner's copies
       mbar_init(bar(kBarPStaged + i), 4);
+      mbar_init(bar(kBarPRecv + i), 1);  // armed each tile (expect_tx 8 KB), completed by the partner's copy
     }
     mbar_init(bar(kBarL), 2);  // the partner's two writer warps
     fence_mbar_init();
@@ -244,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     // an unarmed barrier was measured to stall the copy by ~20 us
     for (int i = 0; i < 2; ++i) {
       mbar_arrive_expect_tx(bar(kBarMax + i), 64 * 4);
+      mbar_arrive_expect_tx(bar(kBarPRecv + i), kPstBytes);
     }
     prefetch_tmap(&p.q_map);
     prefetch_tmap(&p.k_map);
@@ -343,7 +339,6 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       load_v(i - 1);
     }
     load_v(npt - 1);
-    cluster_sync();  // matches the softmax warps' sum exchange
   } else if (warp == 1) {
     // ----------------------------------------------------- UMMA issuer (leader CTA)
     if (rank == 0) {
@@ -426,29 +421,28 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         if (i >= 1) issue_pv((uint32_t)(i - 1), i - 1 == 0);
       }
       issue_pv((uint32_t)(npt - 1), npt == 1);
+      // the last tiles' S-buffer releases (remote arrivals from the partner) land before this CTA can exit:
+      // the final cluster barrier is relaxed
+      for (int j = npt - 2; j < npt; ++j)
+        if (j >= 0) mbar_wait(bar(kBarSFree + (j & 1)), (uint32_t)(j >> 1) & 1);
     }
-    cluster_sync();  // matches the softmax warps' sum exchange
   } else if (warp == kXferWarp) {
     // ----------------------------------------------------- P transfer (each CTA): the staged rows of the
     // partner's heads (8 KB) into rows 128 rank .. of the partner's P half, off the softmax warps' path
     const uint32_t pfull0 = mapa(bar(kBarPFull), 0);
     for (int i = 0; i < npt; ++i) {
-      const uint32_t buf = (uint32_t)i & 1;
-      mbar_wait(bar(kBarPStaged + buf), ((uint32_t)i >> 1) & 1);
-      const uint32_t src = sbase + kOffPst + buf * kPstBytes;
-      const uint32_t dst = mapa(sbase + kOffP + buf * kPBytes + 128 * rank * 64, partner);
-#pragma unroll
-      for (int q = 0; q < kPstBytes / 512; ++q) {
-        const uint32_t off = (q * 32 + lane) * 16;
-        uint32_t a, b, c, d;
-        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(src + off));
-        st_cluster_v4(dst + off, a, b, c, d);
+      const uint32_t buf = (uint32_t)i & 1, ph = ((uint32_t)i >> 1) & 1;
+      mbar_wait(bar(kBarPStaged + buf), ph);
+      if (lane == 0)
+        bulk_copy_to_cluster(mapa(sbase + kOffP + buf * kPBytes + 128 * rank * 64, partner),
+                             sbase + kOffPst + buf * kPstBytes, kPstBytes, mapa(bar(kBarPRecv + buf), partner));
+      mbar_wait_spin(bar(kBarPRecv + buf), ph);  // the partner's rows of this CTA's P half landed
+      if (lane == 0) {
+        if (i + 2 < npt) mbar_arrive_expect_tx(bar(kBarPRecv + buf), kPstBytes);  // tile i + 2, armed ahead
+        mbar_arrive_release_cluster(pfull0 + 8 * buf);
       }
-      fence_proxy_async_cluster();
       __syncwarp();
-      if (lane == 0) mbar_arrive_release_cluster(pfull0 + 8 * buf);
     }
-    cluster_sync();  // matches the softmax warps' sum exchange
   } else {
     // ----------------------------------------------------- softmax (warps 2..9 of both CTAs)
     // TMEM lane quarter wq = warp % 4: S^T lanes = this CTA's keys 32 wq .. 32 wq + 31 of its sub-block; column
@@ -462,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     const float sl2 = p.scale_log2;
     const uint32_t sfree0 = mapa(bar(kBarSFree), 0), pfull0 = mapa(bar(kBarPFull), 0);
     float m_used[32], lpart[32];
+    float m_mine = -INFINITY;  // lane j: running max of head 32 ch + j
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       m_used[j] = -INFINITY;
@@ -484,7 +479,8 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       float wmax_mine = -INFINITY;  // lane j keeps head 32 ch + j
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float x = kvalid ? __uint_as_float(v[j]) : -INFINITY;
+        if (!kvalid) v[j] = __float_as_uint(-INFINITY);
+        const float x = __uint_as_float(v[j]);
         float r;
         asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(x));
         if (j == (int)lane) wmax_mine = r;
@@ -508,24 +504,54 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       if (warp == 2) CTRACE(8, gi);
       const float hmax = fmaxf(cmax, xch[buf * 64 + 32 * ch + lane]) * sl2;  // shared by both CTAs
       uint32_t pk[16];
-      bool any_resc = false;
+      // lane j decides head 32 ch + j (lazy rescale at 2^8); the warp's 32 (-m, corr) pairs are read back as
+      // broadcast float4s instead of 32 shuffles + 32 uniform branches per tile
+      bool any_resc;
       float corr[32];
+      {
+        float* hm = reinterpret_cast<float*>(smem + kOffHm) + (warp - 2) * 64;
+        const bool resc = hmax > m_mine + 8.0f;
+        const float m_new = resc ? hmax : m_mine;
+        const float cr = resc ? ex2(m_mine - m_new) : 1.0f;
+        m_mine = m_new;
+        any_resc = __any_sync(0xffffffffu, resc);
+        __syncwarp();  // the previous tile's reads of this slot are done
+        hm[lane] = -m_new;
+        hm[32 + lane] = cr;
+        __syncwarp();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float tm = __shfl_sync(0xffffffffu, hmax, j);
-        const bool resc = tm > m_used[j] + 8.0f;
-        const float m_new = resc ? tm : m_used[j];
-        corr[j] = resc ? ex2(m_used[j] - m_new) : 1.0f;
-        any_resc |= resc;
-        m_used[j] = m_new;
+        for (int q = 0; q < 8; ++q) {
+          const float4 a = *reinterpret_cast<const float4*>(hm + 4 * q);
+          m_used[4 * q] = a.x;
+          m_used[4 * q + 1] = a.y;
+          m_used[4 * q + 2] = a.z;
+          m_used[4 * q + 3] = a.w;
+        }
+        if (any_resc) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 c = *reinterpret_cast<const float4*>(hm + 32 + 4 * q);
+            corr[4 * q] = c.x;
+            corr[4 * q + 1] = c.y;
+            corr[4 * q + 2] = c.z;
+            corr[4 * q + 3] = c.w;
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) lpart[j] *= corr[j];
+        }
       }
+      {
+        const uint64_t s2 = f2pack(sl2, sl2);
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float e0 = kvalid ? ex2(fmaf(__uint_as_float(v[j]), sl2, -m_used[j])) : 0.f;
-        const float e1 = kvalid ? ex2(fmaf(__uint_as_float(v[j + 1]), sl2, -m_used[j + 1])) : 0.f;
-        lpart[j] = fmaf(lpart[j], corr[j], e0);
-        lpart[j + 1] = fmaf(lpart[j + 1], corr[j + 1], e1);
-        pk[j >> 1] = pack_bf16x2(e0, e1);
+        for (int j = 0; j < 32; j += 2) {  // m_used holds -m here; invalid keys are -inf -> 0
+          float x0, x1;
+          f2unpack(ffma2(f2pack(__uint_as_float(v[j]), __uint_as_float(v[j + 1])), s2, f2pack(m_used[j], m_used[j + 1])),
+                   x0, x1);
+          const float e0 = ex2(x0), e1 = ex2(x1);
+          lpart[j] += e0;
+          lpart[j + 1] += e1;
+          pk[j >> 1] = pack_bf16x2(e0, e1);
+        }
       }
       // P row of CTA ch's half: 64 B = 4 x 16-B units, SWIZZLE_64B (unit ^ (row >> 1) & 3; rows 128 r + kl
       // and kl share the pattern). Own heads: straight into this CTA's P half; the partner's heads: into the
@@ -535,6 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       for (int u = 0; u < 4; ++u)
         st_shared_v4(pr + ((u ^ ((kl >> 1) & 3)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       if (ch != rank) {  // staged for the transfer warp
+        fence_proxy_async_smem();  // the bulk copy (async proxy) reads the staged rows
         __syncwarp();
         if (lane == 0) mbar_arrive_local(bar(kBarPStaged + buf));
       }
@@ -578,82 +605,92 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
       p.trace[11 * 2 * 16 + 8 * 2 * p.batch + 8 * blockIdx.x + (warp - 2)] = g;
     }
-    // ---------------- l[h] = this CTA's keys' sum + the partner's; O^T final once the last PV landed
+    // ---------------- l[h] = this CTA's keys' sum + the partner's (mbarrier swap: no wait for the other roles)
     const uint32_t gl = (uint32_t)(npt - 1);
-    float lmine = 0.f;  // lane j: this warp's key-quarter sum for head 32 ch + j
+    float lmine;  // lane j: this warp's key-quarter sum for head 32 ch + j (transpose-reduce, 31 shuffles)
+    {
+      float v[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      float x = lpart[j];
+      for (int j = 0; j < 32; ++j) v[j] = lpart[j];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (j == (int)lane) lmine = x;
+      for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & (uint32_t)o) != 0;
+#pragma unroll
+        for (int k = 0; k < o; ++k) {
+          const float send = up ? v[k] : v[k + o];
+          const float keep = up ? v[k + o] : v[k];
+          v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      lmine = v[0];
     }
     float* ls = red + ((gl + 1) & 1) * 256;
     ls[wq * 64 + 32 * ch + lane] = lmine;
     named_bar_sync(1, kSmThreads);
     const float lc = (ls[32 * ch + lane] + ls[64 + 32 * ch + lane]) + (ls[128 + 32 * ch + lane] + ls[192 + 32 * ch + lane]);
-    if (wq == 0) st_cluster_f32(mapa(sbase + kOffX + (128 + 32 * ch + lane) * 4, partner), lc);
-    if (warp == 2) CTRACE(10, 0);
-    cluster_sync();  // (all warps of both CTAs) the partner's sums landed
-    GSTAMP(4);
-    if (warp == 2) CTRACE(10, 1);
     if (wq == 0) {
+      st_cluster_f32(mapa(sbase + kOffX + (128 + 32 * ch + lane) * 4, partner), lc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_release_cluster(mapa(bar(kBarL), partner));
+      if (warp == 2) CTRACE(10, 0);
+      mbar_wait_acquire_cluster(bar(kBarL), 0);
       const float lt = lc + xch[128 + 32 * ch + lane];
       const uint32_t h = 32 * ch + lane;
       invl[h] = 1.0f / lt;
-      if (p.lse && rank == 0) p.lse[(int64_t)bi * kH + h] = (m_used_lane(m_used, lane) * 0.69314718055994531f) +
-                                                             __logf(lt);
+      const float mh = m_mine;
+      if (p.lse && rank == 0) p.lse[(int64_t)bi * kH + h] = (mh * 0.69314718055994531f) + __logf(lt);
     }
     mbar_wait(bar(kBarOFull + (gl & 1)), (gl >> 1) & 1);
-    GSTAMP(5);
+    if (warp == 2) CTRACE(10, 1);
     tc_fence_after();
-    named_bar_sync(1, kSmThreads);  // invl written; every P buffer read (the last PV landed): staging is free
-    // O^T (lanes = dims 128 g + 32 wq + lane of this CTA's 256, cols = heads) / l -> bf16 [head][dims] boxes
+    named_bar_sync(1, kSmThreads);  // invl written
+    float w[32];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 w4 = *reinterpret_cast<const float4*>(invl + 32 * ch + 4 * q);
+      w[4 * q] = w4.x;
+      w[4 * q + 1] = w4.y;
+      w[4 * q + 2] = w4.z;
+      w[4 * q + 3] = w4.w;
+    }
+    // O^T (lanes = dims 128 g + 32 wq + lane of this CTA's 256, cols = heads) / l -> O[b][h][dim] straight from
+    // registers: lanes 2d, 2d + 1 swap one value per head pair so each stores two adjacent dims (bf16x2)
     const uint32_t t = 32 * wq + lane;
-    float* ob = reinterpret_cast<float*>(p.o) + (int64_t)bi * p.o_sb + 256 * rank;  // fp32 output only
-#pragma unroll 1
+    const bool even = (lane & 1) == 0;
+    uint32_t ovg[2][32];
+    tmem_ld32(taddr + kTmemO + 32 * ch, ovg[0]);
+    tmem_ld32(taddr + kTmemO + 64 + 32 * ch, ovg[1]);
+    tmem_wait_ld();
+#pragma unroll
     for (int g = 0; g < 2; ++g) {
-      uint32_t ov[32];
-      tmem_ld32(taddr + kTmemO + 64 * g + 32 * ch, ov);
-      tmem_wait_ld();
-      const int dl = 128 * g + (int)t;  // dim within this CTA's 256
-      const uint32_t box = sbase + kOffOut + (dl >> 6) * 8192, col = (uint32_t)(dl & 63);
+      const uint32_t(&ov)[32] = ovg[g];
+      const int gd = 256 * (int)rank + 128 * g + (int)t;  // output dim
+      if (p.out_bf16) {
+        uint16_t* ob = reinterpret_cast<uint16_t*>(p.o) + (int64_t)bi * p.o_sb + (even ? gd : gd - 1);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 w4 = *reinterpret_cast<const float4*>(invl + 32 * ch + 4 * q);
-        const float w[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j = 4 * q + e;
-          const uint32_t h = 32 * ch + j;
-          const float val = __uint_as_float(ov[j]) * w[e];
-          if (p.out_bf16) {
-            const uint32_t a = box + h * 128 + (((col >> 3) ^ (h & 7)) << 4) + (col & 7) * 2;
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)(pack_bf16x2(val, 0.f) & 0xFFFFu)));
-          } else {
-            ob[(int64_t)h * p.o_sh + dl] = val;
-          }
+        for (int j = 0; j < 32; j += 2) {
+          const float a = __uint_as_float(ov[j]) * w[j], c = __uint_as_float(ov[j + 1]) * w[j + 1];
+          const float r = __shfl_xor_sync(0xffffffffu, even ? c : a, 1);
+          const uint32_t pk = even ? pack_bf16x2(a, r) : pack_bf16x2(r, c);
+          const int h = 32 * (int)ch + j + (even ? 0 : 1);
+          asm volatile("st.global.b32 [%0], %1;" ::"l"(ob + (int64_t)h * p.o_sh), "r"(pk) : "memory");
         }
+      } else {
+        float* ob = reinterpret_cast<float*>(p.o) + (int64_t)bi * p.o_sb + gd;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) ob[(int64_t)(32 * ch + j) * p.o_sh] = __uint_as_float(ov[j]) * w[j];
       }
     }
     if (warp == 2) CTRACE(10, 2);
     GSTAMP(6);
-    if (p.out_bf16) {
-      fence_proxy_async_smem();
-      named_bar_sync(1, kSmThreads);
-      if (warp == 2) CTRACE(10, 3);
-      if (warp == 2 && lane == 0) {
-        for (int m = 0; m < 4; ++m) tma_store_3d(&p.o_map, sbase + kOffOut + m * 8192, 256 * (int)rank + 64 * m, 0, bi);
-        bulk_commit_group();
-        bulk_wait_group_read0();
-      }
-    }
   }
   __syncwarp();
   if (warp == 2) CTRACE(10, 4);
   GSTAMP(7);
   tc_fence_before();
-  cluster_sync();  // every DSMEM write landed before either CTA's shared memory goes away
+  // every remote access into either CTA was awaited by its target (mbarrier phases above), so the barrier only
+  // orders exits and the TMEM dealloc after both CTAs' last TMEM reads: relaxed, the O stores need not drain
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
   if (warp == 2) CTRACE(10, 5);
   if (p.trace && threadIdx.x == 64) {
     unsigned long long g;
@@ -723,7 +760,6 @@ cudaError_t launch_decode_coop(const AttnProblem& a, int32_t* status, cudaStream
   if (!encode_3d(&p.k_map, s.k, kDqk, (uint64_t)a.n_kv, a.batch, s.k_st, s.k_sb, 128)) return cudaErrorInvalidValue;
   if (!encode_4d_chunks(&p.v_map, s.v, kDv, (uint64_t)a.n_kv, a.batch, s.v_st, s.v_sb, 32, 4))
     return cudaErrorInvalidValue;
-  if (a.out_bf16 && !encode_3d(&p.o_map, a.o, kDv, kH, a.batch, a.o_sh, a.o_sb, 64)) return cudaErrorInvalidValue;
   // per launch (the attribute is per device; a process may drive several GPUs)
   cudaError_t ea = cudaFuncSetAttribute(decode_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
   if (ea != cudaSuccess) return ea;
