@@ -17,8 +17,11 @@
 //    sums l are swapped once at the end through an mbarrier (the other roles do not wait); each CTA
 //    normalises its own dims and stores them straight from registers (lane pairs swap one value per head pair
 //    so every store is a bf16x2); the final cluster barrier is relaxed (no wait for the stores to drain).
+//  * S runs two tiles ahead of PV (MMA order S(0), S(1), S(2), PV(0), S(3), PV(1), ..., three S^T buffers in
+//    TMEM) so the HBM-bound K rows of tile i + 2 are in flight while P(i) is being made; the softmax of tile i
+//    waits for PV(i - 2) before it rewrites that tile's P buffer and staging block.
 //  * Loads: warp 0 of each CTA (Q halves first through 9 chunk barriers; then a ring of 4 x 32 KB items in
-//    MMA order K(0), K(1), V(0), K(2), V(1), ...; pair TMA with completion on the leader's barriers);
+//    MMA order K(0), K(1), K(2), V(0), K(3), V(1), ...; pair TMA with completion on the leader's barriers);
 //    warp 1 of the leader issues every UMMA; warps 2-9 of both CTAs run the softmax.
 #include <math.h>
 #include <stdlib.h>
@@ -53,9 +56,10 @@ constexpr int kOffBar = kOffRing + kStages * kStageBytes;
 constexpr int kBarFull = 0;
 constexpr int kBarEmpty = kBarFull + kStages;
 constexpr int kBarQFull = kBarEmpty + kStages;    // [9]
-constexpr int kBarSFull = kBarQFull + kChunks;    // [2]
-constexpr int kBarSFree = kBarSFull + 2;          // [2]
-constexpr int kBarPFull = kBarSFree + 2;          // [2]
+constexpr int kSBufs = 3;                         // S^T buffers in TMEM (S runs two tiles ahead of PV)
+constexpr int kBarSFull = kBarQFull + kChunks;    // [kSBufs]
+constexpr int kBarSFree = kBarSFull + kSBufs;     // [kSBufs]
+constexpr int kBarPFull = kBarSFree + kSBufs;     // [2]
 constexpr int kBarOFull = kBarPFull + 2;          // [2]
 constexpr int kBarMax = kBarOFull + 2;            // [2] partner's tile maxima landed (bulk copy, local)
 constexpr int kBarPStaged = kBarMax + 2;          // [2] the partner's-heads P rows are staged (4 warps, local)
@@ -72,7 +76,7 @@ constexpr int kSmemUsed = kOffHm + 8 * 64 * 4;
 constexpr int kSmemAlloc = kSmemUsed;
 static_assert(kSmemAlloc <= 232448, "smem");
 
-constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kTmemO = 0, kTmemS = 128;  // O^T group g at 64 g (lanes = dims), S^T buffer b at 128 + 64 b
 constexpr uint32_t kSoftmaxWarps = 8;
 constexpr uint32_t kSmThreads = 32 * kSoftmaxWarps;
@@ -105,6 +109,9 @@ struct CoopParams {
       p.trace[((slot) * 2 + cluster_ctarank()) * 16 + (idx)] = clock64();                       \
   } while (0)
 
+// S^T buffer of tile gi and the parity of its use
+__device__ __forceinline__ uint32_t sbuf(uint32_t gi) { return gi % 3; }
+__device__ __forceinline__ uint32_t sphase(uint32_t gi) { return (gi / 3) & 1; }
 struct SeqTiles {
   int32_t n_sink, loc_begin, n_tiles;  // selected 128-key sub-blocks
   int32_t pos;
@@ -226,6 +233,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(kBarSFull + i), 1);
       mbar_init(bar(kBarSFree + i), kArrivalsPerPair);
+      if (i == 1) {
+        mbar_init(bar(kBarSFull + 2), 1);
+        mbar_init(bar(kBarSFree + 2), kArrivalsPerPair);
+      }
       mbar_init(bar(kBarPFull + i), kPFullArrivals);
       mbar_init(bar(kBarOFull + i), 1);
       mbar_init(bar(kBarMax + i), 1);    // armed each tile (expect_tx 256 B), completed by the partner's copies
@@ -334,11 +345,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       }
     };
     load_k(0);
-    for (int i = 1; i < npt; ++i) {
-      load_k(i);
-      load_v(i - 1);
+    if (npt > 1) load_k(1);
+    for (int i = 0; i < npt; ++i) {
+      if (i + 2 < npt) load_k(i + 2);
+      load_v(i);
     }
-    load_v(npt - 1);
   } else if (warp == 1) {
     // ----------------------------------------------------- UMMA issuer (leader CTA)
     if (rank == 0) {
@@ -356,9 +367,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         }
       };
       auto issue_s = [&](uint32_t gi) {
-        const uint32_t buf = gi & 1;
+        const uint32_t buf = sbuf(gi);
         CTRACE(1, gi);
-        mbar_wait(bar(kBarSFree + buf), ((gi >> 1) & 1) ^ 1);
+        mbar_wait(bar(kBarSFree + buf), sphase(gi) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + kTmemS + 64 * buf;
         for (int j = 0; j < (kChunks + 1) / 2; ++j) {
@@ -416,15 +427,16 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         __syncwarp();
         CTRACE(5, gi);
       };
+      issue_s(0);
+      if (npt > 1) issue_s(1);
       for (int i = 0; i < npt; ++i) {
-        issue_s((uint32_t)i);
-        if (i >= 1) issue_pv((uint32_t)(i - 1), i - 1 == 0);
+        if (i + 2 < npt) issue_s((uint32_t)(i + 2));
+        issue_pv((uint32_t)i, i == 0);
       }
-      issue_pv((uint32_t)(npt - 1), npt == 1);
       // the last tiles' S-buffer releases (remote arrivals from the partner) land before this CTA can exit:
       // the final cluster barrier is relaxed
-      for (int j = npt - 2; j < npt; ++j)
-        if (j >= 0) mbar_wait(bar(kBarSFree + (j & 1)), (uint32_t)(j >> 1) & 1);
+      for (int j = npt - kSBufs; j < npt; ++j)
+        if (j >= 0) mbar_wait(bar(kBarSFree + sbuf((uint32_t)j)), sphase((uint32_t)j));
     }
   } else if (warp == kXferWarp) {
     // ----------------------------------------------------- P transfer (each CTA): the staged rows of the
@@ -463,18 +475,18 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       lpart[j] = 0.f;
     }
     for (int i = 0; i < npt; ++i) {
-      const uint32_t gi = (uint32_t)i, buf = gi & 1;
+      const uint32_t gi = (uint32_t)i, buf = gi & 1, sb = sbuf(gi);
       const int32_t kb0 = sub_k0(st, 2 * i + (int)rank);
       const bool kvalid = kb0 >= 0 && kb0 + (int32_t)kl <= st.pos;
-      mbar_wait(bar(kBarSFull + buf), (gi >> 1) & 1);
+      mbar_wait(bar(kBarSFull + sb), sphase(gi));
       if (warp == 2) CTRACE(6, gi);
       tc_fence_after();
       uint32_t v[32];
-      tmem_ld32(taddr + kTmemS + 64 * buf + 32 * ch, v);
+      tmem_ld32(taddr + kTmemS + 64 * sb + 32 * ch, v);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(sfree0 + 8 * buf);
+      if (lane == 0) mbar_arrive_cluster(sfree0 + 8 * sb);
       float* rb = red + buf * 256;
       float wmax_mine = -INFINITY;  // lane j keeps head 32 ch + j
 #pragma unroll
@@ -556,6 +568,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       // P row of CTA ch's half: 64 B = 4 x 16-B units, SWIZZLE_64B (unit ^ (row >> 1) & 3; rows 128 r + kl
       // and kl share the pattern). Own heads: straight into this CTA's P half; the partner's heads: into the
       // staging block that one bulk DSMEM copy moves to rows 128 rank .. of the partner's half.
+      // S(i) completing no longer implies PV(i - 2) completed (S runs two tiles ahead): the P buffer and the
+      // staging block of tile i - 2 are free once PV(i - 2) has landed
+      if (i >= 2) mbar_wait(bar(kBarOFull + (buf)), ((gi - 2) >> 1) & 1);
       const uint32_t pr = ch == rank ? sbase + kOffP + buf * kPBytes + prow * 64 : sbase + kOffPst + buf * kPstBytes + kl * 64;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -565,8 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_local(bar(kBarPStaged + buf));
       }
-      // O^T rescale once PV(i - 1) has landed -- only when a head's max moved (the P buffer written above is
-      // free without a wait: S(i) completing implies PV(i - 2) completed, the tensor pipe being in order)
+      // O^T rescale once PV(i - 1) has landed -- only when a head's max moved
       if (i > 0 && __any_sync(0xffffffffu, any_resc)) {  // corr is per head: uniform across a warp with this ch
         const uint32_t gp = gi - 1;
         mbar_wait(bar(kBarOFull + (gp & 1)), (gp >> 1) & 1);
