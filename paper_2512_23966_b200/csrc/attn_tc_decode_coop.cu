@@ -56,7 +56,10 @@ constexpr int kOffBar = kOffRing + kStages * kStageBytes;
 constexpr int kBarFull = 0;
 constexpr int kBarEmpty = kBarFull + kStages;
 constexpr int kBarQFull = kBarEmpty + kStages;    // [9]
-constexpr int kSBufs = 3;                         // S^T buffers in TMEM (S runs two tiles ahead of PV)
+// S runs kAhead tiles ahead of PV. Measured (B64 at 128K, bench timing): 1 (FA order) 22.2 us, 2 21.1-21.2,
+// 3 21.85, 4 21.98 -- beyond 2 the V re-reads bunch up behind the last K tile
+constexpr int kAhead = 2;
+constexpr int kSBufs = kAhead + 1;                // S^T buffers in TMEM
 constexpr int kBarSFull = kBarQFull + kChunks;    // [kSBufs]
 constexpr int kBarSFree = kBarSFull + kSBufs;     // [kSBufs]
 constexpr int kBarPFull = kBarSFree + kSBufs;     // [2]
@@ -110,8 +113,8 @@ struct CoopParams {
   } while (0)
 
 // S^T buffer of tile gi and the parity of its use
-__device__ __forceinline__ uint32_t sbuf(uint32_t gi) { return gi % 3; }
-__device__ __forceinline__ uint32_t sphase(uint32_t gi) { return (gi / 3) & 1; }
+__device__ __forceinline__ uint32_t sbuf(uint32_t gi) { return gi % kSBufs; }
+__device__ __forceinline__ uint32_t sphase(uint32_t gi) { return (gi / kSBufs) & 1; }
 struct SeqTiles {
   int32_t n_sink, loc_begin, n_tiles;  // selected 128-key sub-blocks
   int32_t pos;
@@ -230,13 +233,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       mbar_init(bar(kBarEmpty + i), 1);
     }
     for (int i = 0; i < kChunks; ++i) mbar_init(bar(kBarQFull + i), 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSBufs; ++i) {
       mbar_init(bar(kBarSFull + i), 1);
       mbar_init(bar(kBarSFree + i), kArrivalsPerPair);
-      if (i == 1) {
-        mbar_init(bar(kBarSFull + 2), 1);
-        mbar_init(bar(kBarSFree + 2), kArrivalsPerPair);
-      }
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(bar(kBarPFull + i), kPFullArrivals);
       mbar_init(bar(kBarOFull + i), 1);
       mbar_init(bar(kBarMax + i), 1);    // armed each tile (expect_tx 256 B), completed by the partner's copies
@@ -344,10 +345,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         next();
       }
     };
-    load_k(0);
-    if (npt > 1) load_k(1);
+    for (int i = 0; i < kAhead && i < npt; ++i) load_k(i);
     for (int i = 0; i < npt; ++i) {
-      if (i + 2 < npt) load_k(i + 2);
+      if (i + kAhead < npt) load_k(i + kAhead);
       load_v(i);
     }
   } else if (warp == 1) {
@@ -427,10 +427,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         __syncwarp();
         CTRACE(5, gi);
       };
-      issue_s(0);
-      if (npt > 1) issue_s(1);
+      for (int i = 0; i < kAhead && i < npt; ++i) issue_s((uint32_t)i);
       for (int i = 0; i < npt; ++i) {
-        if (i + 2 < npt) issue_s((uint32_t)(i + 2));
+        if (i + kAhead < npt) issue_s((uint32_t)(i + kAhead));
         issue_pv((uint32_t)i, i == 0);
       }
       // the last tiles' S-buffer releases (remote arrivals from the partner) land before this CTA can exit:
