@@ -134,3 +134,40 @@ def test_ssa_decode_large_batch(B):
         ref, _ = _oracle_decode(qs, ks, bi, seq[bi], pattern)
         got = o[bi, 0].double().cpu().numpy()
         assert np.abs(got - ref).max() <= MAXABS, (bi, seq[bi], np.abs(got - ref).max())
+
+
+@pytest.mark.parametrize("pattern,heads", [((1, 7, 128), 64), ((2, 3, 256), 64), ((1, 7, 128), 32)])
+def test_ssa_decode_rescale_in_later_tiles(pattern, heads):
+    """The running per-head max grows past the lazy-rescale threshold (2^8) twice after the first tile: the
+    RoPE column of every query and of the keys of two later selected blocks is raised (host-side input
+    construction from the numpy generator twin), so O^T and the row sums are rescaled in tiles >= 2 while S runs
+    ahead of PV (H = 64: the pair-cooperative kernel; H = 32: the key-split kernel of a head-sharded GPU).
+    Eq. 4 against the fp64 oracle on exactly the uploaded bf16 values."""
+    s, l, b = pattern
+    B, T, Hh = 3, 4096, heads
+    qs = Spec(seed=21, tensor_id=TID_Q, batch=B, n=1, heads=Hh, d=D_QK)
+    ks = Spec(seed=21, tensor_id=TID_K, batch=B, n=T, heads=1, d=D_QK)
+    qf = gen_rows_f32(qs, 0, B * Hh).reshape(B, Hh, D_QK)
+    kf = gen_rows_f32(ks, 0, B * T).reshape(B, T, D_QK)
+    seq = [T, T - 100, 3000]
+    qf[:, :, D_QK - 1] += 12.0
+    for bi, L in enumerate(seq):
+        qb = (L - 1) // b
+        lo = max(s, qb - l + 1)  # first local block
+        mid = lo + (qb - lo) // 2
+        kf[bi, mid * b:(mid + 1) * b, D_QK - 1] += 12.0  # a later tile: the max jumps by ~144 scale log2(e) ~ 15
+        kf[bi, qb * b:L, D_QK - 1] += 20.0               # the last block: jumps again (~25)
+    q = torch.from_numpy(qf).to(torch.bfloat16).reshape(B, 1, Hh, D_QK).cuda()
+    cache = torch.from_numpy(kf).to(torch.bfloat16).cuda()
+    qh = q.float().cpu().numpy().astype(np.float64).reshape(B, Hh, D_QK)
+    kh = cache.float().cpu().numpy().astype(np.float64)
+    sl = torch.tensor(seq, dtype=torch.int32, device="cuda")
+    lse = torch.full((B, Hh, 1), float("nan"), device="cuda")
+    o = loza.ssa_decode(q, cache, sl, pattern=pattern, scale=SCALE, out_dtype=torch.float32, lse=lse)
+    torch.cuda.synchronize()
+    for bi, L in enumerate(seq):
+        keys = oracle.allowed_keys(L - 1, L, s, l, b)
+        ref, rl = oracle.attend(qh[bi], kh[bi, keys], kh[bi, keys][:, :D_V], SCALE)
+        got = o[bi, 0].double().cpu().numpy()
+        assert np.abs(got - ref).max() <= MAXABS, (bi, L, np.abs(got - ref).max())
+        assert np.abs(lse[bi, :, 0].double().cpu().numpy() - rl).max() <= 1e-3 * max(1, np.abs(rl).max())
