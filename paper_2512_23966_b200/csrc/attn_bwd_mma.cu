@@ -694,9 +694,14 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
   const bool force_mma = knob(kKnobBackward) == 2;
   const bool force_dq_mma = knob(kKnobBackward) == 3;
   const bool tc_keys = !force_mma && backward_tc_eligible(a, dout);
+  // 64-key tiles (a dV kernel and a dK kernel, attn_bwd_tc.cu) unless the tile would straddle a block or the
+  // test knob backward = 4 keeps the 32-key kernel that accumulates dK and dV in one pass
+  const bool key64 = knob(kKnobBackward) != 4 && backward_key64_eligible(a);
   if (tc_keys && !force_dq_mma && ds && backward_ds_eligible(a) && rows > 0 && a.n_kv > 0) {
     if ((e = launch_bwd_D(a, dout, D, st)) != cudaSuccess) return e;
-    if ((e = launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st)) != cudaSuccess) return e;
+    e = key64 ? launch_bwd_key64_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st)
+              : launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st);
+    if (e != cudaSuccess) return e;
     if ((e = launch_bwd_dq_tc(a, ds, dq, st)) != cudaSuccess) return e;
     if (use_part) {
       const int64_t n = (int64_t)a.batch * p.n_sink * kKKeys * (kDKV / 4);
@@ -714,7 +719,8 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
   }
   if (a.n_kv > 0) {
     if (tc_keys) {
-      e = launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, nullptr, p.nsplit, p.n_sink, st);
+      e = key64 ? launch_bwd_key64_tc(a, dout, dk, dv, D, part, nullptr, p.nsplit, p.n_sink, st)
+                : launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, nullptr, p.nsplit, p.n_sink, st);
       if (e != cudaSuccess) return e;
     } else {
       e = cudaFuncSetAttribute(bwd_dkdv_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKSmem);

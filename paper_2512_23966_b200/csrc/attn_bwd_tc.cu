@@ -409,6 +409,343 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
   }
 }
 
+// ------------------------------------------------------------------------------ key side, 64-key tiles
+// The 32-key kernel above holds dK^T and dV^T of its keys in TMEM (288 columns) and so streams every row tile
+// past 32 keys, twice. Here the key side is split into two kernels over 64-key tiles, each with one
+// accumulator (MODE kDvOnly: dV^T = dO^T P, 4 x 64 columns; MODE kDkOnly: dK^T = Q^T dS, 5 x 64 columns):
+//   dV kernel: S = Q K^T (Q pairs once), P = exp2(S scale log2e - LSE log2e), dV^T += dO^T P (dO pairs once)
+//   dK kernel: S = Q K^T, dP = dO V^T (Q, dO pairs), dS = P (dP - D), dK^T += Q^T dS (Q pairs again); it also
+//              writes the dS rows the dQ GEMM reads.
+// Per 128-row tile and 64 keys the two kernels move Q 3x + dO 2x (703 KB) where the 32-key kernel moves
+// Q 4x + dO 4x (1112 KB), and every UMMA is M128 N64 (48 tensor cycles) instead of M128 N32.
+// TMEM: dV kernel dV^T 256 + S 2 x 64; dK kernel dK^T 320 + S 64 + dP 64 (single-buffered: the P/dS warps
+// release them right after their TMEM loads). SMEM: ring 4 x 32 KB, K tile 72 KB, P or dS 16 KB (SW128).
+constexpr int kDvOnly = 1, kDkOnly = 2;
+constexpr int k64Keys = 64;
+constexpr int k64Stages = 4;
+constexpr int k64KBytes = 9 * k64Keys * 128;       // 72 KB: [9 chunks][64 keys][64]
+constexpr int k64PBytes = kRows * 128;             // [128 rows][64 keys] bf16, SWIZZLE_128B
+constexpr int k64OffRing = 0;
+constexpr int k64OffK = k64OffRing + k64Stages * kPairBytes;
+constexpr int k64OffP = k64OffK + k64KBytes;
+constexpr int k64OffBar = k64OffP + k64PBytes;
+constexpr int k64BarFull = 0, k64BarEmpty = k64Stages, k64BarK = 2 * k64Stages, k64BarSFull = k64BarK + 1,
+              k64BarSFree = k64BarSFull + 2, k64BarPReady = k64BarSFree + 2, k64BarPFree = k64BarPReady + 1,
+              k64BarAcc = k64BarPFree + 1, k64NumBars = k64BarAcc + 1;
+constexpr int k64OffTmemPtr = k64OffBar + 8 * k64NumBars;
+constexpr int k64Smem = k64OffTmemPtr + 16 + 1024;
+static_assert(k64Smem <= 232448, "smem");
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_constant__ TcBwdParams p) {
+  constexpr bool kIsDv = MODE == kDvOnly;
+  constexpr int kSBufs = kIsDv ? 2 : 1;  // S (and dP) buffers in TMEM
+  constexpr uint32_t kTmemAcc = 0;                     // dV^T: 4 x 64 columns, dK^T: 5 x 64
+  constexpr uint32_t kTmemS = kIsDv ? 256 : 320, kTmemDP = 384;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sbase - sraw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = p.heads;
+  const int ktiles = (p.n_kv + k64Keys - 1) / k64Keys;
+  const int bi = blockIdx.x / ktiles, tile = blockIdx.x - bi * ktiles, j0 = tile * k64Keys;
+  // rows attending keys [j0, j0 + 64) (b % 64 == 0: the tile lies in one block)
+  int p0 = p.causal ? j0 : 0, p1 = p.q_start + p.n_q;
+  const int kb = j0 / p.b;
+  if (p.sparse && kb >= p.s) {
+    const int pe = (kb + p.l) * p.b;
+    if (pe < p1) p1 = pe;
+  }
+  if (p0 < p.q_start) p0 = p.q_start;
+  int R0 = 0, R1 = 0;
+  if (p1 > p0) {
+    R0 = (p0 - p.q_start) * H;
+    R1 = (p1 - p.q_start) * H;
+  }
+  const bool split = p.sparse && kb < p.s && p.nsplit > 1;
+  if (split) {
+    const int chunk = ((R1 - R0 + p.nsplit - 1) / p.nsplit + kRows - 1) / kRows * kRows;
+    const int a = R0 + (int)blockIdx.y * chunk, e = a + chunk;
+    R0 = a < R1 ? a : R1;
+    R1 = e < R1 ? e : R1;
+  } else if (blockIdx.y > 0) {
+    return;
+  }
+  RowIter it;
+  it.L = p.sparse && !split && kb >= p.s ? p.l : 1;
+  it.m0 = p0 / p.b;
+  it.m1 = (p1 - 1) / p.b;
+  it.p0 = p0;
+  it.p1 = p1;
+  it.R0 = R0;
+  it.R1 = R1;
+  it.qs = p.q_start;
+  it.H = H;
+  it.b = p.b;
+  it.start();
+  const bool any = it.valid();
+
+  auto bar = [&](int i) { return sbase + k64OffBar + 8 * i; };
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + k64OffTmemPtr);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < k64Stages; ++i) {
+      mbar_init(bar(k64BarFull + i), 1);
+      mbar_init(bar(k64BarEmpty + i), 1);
+    }
+    mbar_init(bar(k64BarK), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(k64BarSFull + i), 1);
+      mbar_init(bar(k64BarSFree + i), 4);
+    }
+    mbar_init(bar(k64BarPReady), 4);
+    mbar_init(bar(k64BarPFree), 1);
+    mbar_init(bar(k64BarAcc), 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.q_map);
+    prefetch_tmap(&p.o_map);
+    prefetch_tmap(&p.k_map);
+  }
+  if (warp == 1) tmem_alloc<1>(smem_u32(tmem_ptr), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0 && any) {
+      const uint64_t pol_k = policy_evict_last(), pol = policy_evict_normal();
+      mbar_arrive_expect_tx(bar(k64BarK), k64KBytes);
+      tma_load_4d(sbase + k64OffK, &p.k_map, 0, j0, 0, bi, bar(k64BarK), pol_k);
+      uint32_t slot = 0, ph = 0;
+      auto load_pair = [&](const CUtensorMap* m, int pair, int rb) {
+        mbar_wait(bar(k64BarEmpty + slot), ph ^ 1);
+        mbar_arrive_expect_tx(bar(k64BarFull + slot), kPairBytes);
+        tma_load_4d(sbase + k64OffRing + slot * kPairBytes, m, 0, rb, 2 * pair, bi, bar(k64BarFull + slot), pol);
+        if (++slot == k64Stages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      };
+      // the UMMA issuer's order: the first pass (S, and dP) of tile t + 1 before the gradient pass of tile t
+      auto load_first = [&](int rb) {
+        for (int q = 0; q < kQPairs; ++q) load_pair(&p.q_map, q, rb);
+        if (!kIsDv)
+          for (int q = 0; q < kOPairs; ++q) load_pair(&p.o_map, q, rb);
+      };
+      auto load_grad = [&](int rb) {
+        if (kIsDv)
+          for (int q = 0; q < kOPairs; ++q) load_pair(&p.o_map, q, rb);
+        else
+          for (int q = 0; q < kQPairs; ++q) load_pair(&p.q_map, q, rb);
+      };
+      RowIter ia = it;
+      load_first(ia.rb);
+      ia.advance();
+      for (; it.valid(); it.advance()) {
+        if (ia.valid()) {
+          load_first(ia.rb);
+          ia.advance();
+        }
+        load_grad(it.rb);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ UMMA issuer
+    if (any) {
+      constexpr uint32_t id_s = idesc_bf16_f32(kRows, k64Keys, false, false);
+      constexpr uint32_t id_t = idesc_bf16_f32(128, k64Keys, true, true);
+      mbar_wait(bar(k64BarK), 0);
+      tc_fence_after();
+      uint32_t slot = 0, ph = 0;
+      auto take = [&]() {
+        mbar_wait(bar(k64BarFull + slot), ph);
+        tc_fence_after();
+      };
+      auto release = [&]() {
+        if (elect_one()) umma_commit_1sm(bar(k64BarEmpty + slot));
+        __syncwarp();
+        if (++slot == k64Stages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      };
+      // S (and dP) of tile t + 1 are issued before the gradient UMMAs of tile t
+      auto issue_first = [&](int tc) {
+        const int buf = tc % kSBufs, use = tc / kSBufs;
+        mbar_wait(bar(k64BarSFree + buf), (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tS = tmem + kTmemS + 64 * buf;
+        for (int q = 0; q < kQPairs; ++q) {  // S = Q K^T
+          take();
+          if (elect_one()) {
+            const int nk = q < kQPairs - 1 ? 8 : 4;
+            for (int k = 0; k < nk; ++k) {
+              const uint32_t ch = 2 * q + (k >> 2), kk = k & 3;
+              umma_bf16_1sm(tS, sdesc_sw128(sbase + k64OffRing + slot * kPairBytes + (k >> 2) * 16384 + 32 * kk, 16, 1024),
+                            sdesc_sw128(sbase + k64OffK + ch * (k64Keys * 128) + 32 * kk, 16, 1024), id_s, (q | k) != 0);
+            }
+          }
+          release();
+        }
+        if (!kIsDv) {
+          for (int q = 0; q < kOPairs; ++q) {  // dP = dO V^T (V = K[:, :512])
+            take();
+            if (elect_one()) {
+              for (int k = 0; k < 8; ++k) {
+                const uint32_t ch = 2 * q + (k >> 2), kk = k & 3;
+                umma_bf16_1sm(tmem + kTmemDP,
+                              sdesc_sw128(sbase + k64OffRing + slot * kPairBytes + (k >> 2) * 16384 + 32 * kk, 16, 1024),
+                              sdesc_sw128(sbase + k64OffK + ch * (k64Keys * 128) + 32 * kk, 16, 1024), id_s,
+                              (q | k) != 0);
+              }
+            }
+            release();
+          }
+        }
+        if (elect_one()) umma_commit_1sm(bar(k64BarSFull + buf));
+        __syncwarp();
+      };
+      auto issue_grad = [&](int tc) {
+        mbar_wait(bar(k64BarPReady), tc & 1);
+        tc_fence_after();
+        const uint32_t pb = sbase + k64OffP;
+        const int np = kIsDv ? kOPairs : kQPairs;  // dV^T[dims 128 q ..] += dO^T P  /  dK^T[..] += Q^T dS
+        for (int q = 0; q < np; ++q) {
+          take();
+          if (elect_one()) {
+            for (int kr = 0; kr < 8; ++kr)
+              umma_bf16_1sm(tmem + kTmemAcc + 64 * q,
+                            sdesc_sw128(sbase + k64OffRing + slot * kPairBytes + 2048 * kr, 16384, 1024),
+                            sdesc_sw128(pb + 2048 * kr, 16, 1024), id_t, (tc | kr) != 0);
+          }
+          release();
+        }
+        if (elect_one()) umma_commit_1sm(bar(k64BarPFree));
+        __syncwarp();
+      };
+      RowIter ia = it;
+      issue_first(0);
+      ia.advance();
+      int ta = 1;
+      for (int tc = 0; it.valid(); it.advance(), ++tc) {
+        if (ia.valid()) {
+          issue_first(ta++);
+          ia.advance();
+        }
+        issue_grad(tc);
+      }
+      if (elect_one()) umma_commit_1sm(bar(k64BarAcc));
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ P or dS (thread = row = TMEM lane)
+    const int q = warp - 4, row = 32 * q + lane;
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+    const int rows = p.n_q * H;
+    const bool jsink = !p.sparse || kb < p.s;
+    for (int tc = 0; it.valid(); it.advance(), ++tc) {
+      const int buf = tc % kSBufs, use = tc / kSBufs;
+      const int r = it.rb + row;
+      const bool rv = r < it.re;
+      const int rr = rv ? r : 0, t = div_h(p, rr), h = rr - t * H, pos = p.q_start + t;
+      const float lse2 = rv ? p.lse[((int64_t)bi * H + h) * p.n_q + t] * kLog2e : 0.f;
+      const float Dr = (!kIsDv && rv) ? p.D[(int64_t)bi * rows + rr] : 0.f;
+      const bool win = jsink || kb >= pos / p.b - p.l + 1;
+      mbar_wait(bar(k64BarSFull + buf), use & 1);
+      tc_fence_after();
+      uint32_t pk[32];
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {  // keys 32 hf .. 32 hf + 31
+        uint32_t sv[32], dv[32];
+        tmem_ld32(tl + kTmemS + 64 * buf + 32 * hf, sv);
+        if (!kIsDv) tmem_ld32(tl + kTmemDP + 32 * hf, dv);
+        tmem_wait_ld();
+        if (hf == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_local(bar(k64BarSFree + buf));
+        }
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          float v2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = j0 + 32 * hf + c + e;
+            const bool ok = rv && win && j < p.n_kv && (!p.causal || j <= pos);
+            const float pv = ok ? ex2(fmaf(__uint_as_float(sv[c + e]), p.sl2, -lse2)) : 0.f;
+            v2[e] = kIsDv ? pv : pv * (__uint_as_float(dv[c + e]) - Dr);
+          }
+          pk[16 * hf + (c >> 1)] = pack_bf16x2(v2[0], v2[1]);
+        }
+      }
+      if (!kIsDv && p.ds && rv) {  // this row's 64 dS values at its slots of block kb
+        int lbq = pos / p.b - p.l + 1;
+        if (lbq < p.s) lbq = p.s;
+        const int W = (p.s + p.l) * p.b;
+        const int slot = kb < p.s ? j0 : p.s * p.b + (kb - lbq) * p.b + (j0 - kb * p.b);
+        uint4* dst = reinterpret_cast<uint4*>(p.ds + ((int64_t)bi * rows + rr) * W + slot);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      }
+      mbar_wait(bar(k64BarPFree), (tc & 1) ^ 1);
+      // row of 128 B = 8 x 16-B units, SWIZZLE_128B: unit u at (u ^ row & 7)
+      const uint32_t pr = sbase + k64OffP + row * 128;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        st_shared_v4(pr + (uint32_t)((u ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(bar(k64BarPReady));
+    }
+    // ------------------------------------------------------------------ epilogue: TMEM lane = dim, column = key
+    if (any) {
+      mbar_wait(bar(k64BarAcc), 0);
+      tc_fence_after();
+    }
+    const int nm = kIsDv ? kOPairs : kQPairs;
+    for (int m = 0; m < nm; ++m) {
+      const int dim = 128 * m + 32 * q + lane;
+      if (!kIsDv && 128 * m + 32 * q >= kDqk) continue;  // warp-uniform: dims 576.. of the last dK^T tile
+      const float sc = kIsDv ? 1.f : p.scale;
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t v[32];
+        if (any) {
+          tmem_ld32(tl + kTmemAcc + 64 * m + 32 * hf, v);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) v[c] = 0u;
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int j = j0 + 32 * hf + c;
+          if (j >= p.n_kv) continue;
+          const float x = __uint_as_float(v[c]) * sc;
+          if (split) {  // partials in the 32-key tile layout of the sink reduce: [B][n_sink][nsplit][32][1088]
+            const int t32 = j >> 5, kl = j & 31;
+            p.part[((((int64_t)bi * p.n_sink + t32) * p.nsplit + blockIdx.y) * kKeys + kl) * kDkv + (kIsDv ? kDqk : 0) + dim] = x;
+          } else if (kIsDv) {
+            p.dv[((int64_t)bi * p.n_kv + j) * kDv + dim] = x;
+          } else {
+            p.dk[((int64_t)bi * p.n_kv + j) * kDqk + dim] = x;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<1>(tmem, 512);
+  }
+}
+
 // ---------------------------------------------------------------------------------------------- dQ = dS K
 // SSA only: dQ[128 rows, 192-dim slice] = scale * DS[rows, slots] K[slots -> keys, slice] as a tcgen05 GEMM
 // (M128 N192 K16, A = DS K-major, B = K MN-major over 3 64-dim atoms) from the dS rows the key kernel wrote:
@@ -668,6 +1005,58 @@ cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk
   const int64_t kt = (a.n_kv + kKeys - 1) / kKeys;
   const bool use_part = a.sparse && nsplit > 1;
   bwd_dkdv_tc_kernel<<<dim3((unsigned)(a.batch * kt), use_part ? nsplit : 1), 256, kSmem, st>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// 64-key tiles (two kernels, dV then dK): the tile must lie in one block (b % 64 == 0) when sparse
+bool backward_key64_eligible(const AttnProblem& a) { return !a.sparse || a.b % k64Keys == 0; }
+
+cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
+                                float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st) {
+  TcBwdParams p;
+  const auto& kv = a.kv.seg[0];
+  const uint64_t rows = (uint64_t)a.n_q * a.heads;
+  if (!encode_4d_chunks(&p.q_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 2) ||
+      !encode_4d_chunks(&p.o_map, dout, kDv, rows, a.batch, a.o_sh, a.o_sb, kRows, 2) ||
+      !encode_4d_chunks(&p.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, k64Keys, 9))
+    return cudaErrorInvalidValue;
+  p.lse = a.lse;
+  p.D = D;
+  p.dk = dk;
+  p.dv = dv;
+  p.part = part;
+  p.ds = ds;
+  p.batch = a.batch;
+  p.n_q = a.n_q;
+  p.heads = a.heads;
+  p.n_kv = (int32_t)a.n_kv;
+  p.q_start = (int32_t)a.q_start;
+  p.scale = a.scale;
+  p.sl2 = a.scale * kLog2e;
+  p.sparse = a.sparse;
+  p.causal = a.causal;
+  p.s = a.s;
+  p.l = a.l;
+  p.b = a.b;
+  p.nsplit = nsplit;
+  p.n_sink = n_sink;
+  {
+    uint32_t l = 0;
+    while ((1ull << l) < (uint64_t)a.heads) ++l;
+    p.h_p = 31 + l;
+    p.h_m = (uint32_t)(((1ull << p.h_p) + a.heads - 1) / a.heads);
+  }
+  const int64_t kt = (a.n_kv + k64Keys - 1) / k64Keys;
+  const bool use_part = a.sparse && nsplit > 1;
+  const dim3 grid((unsigned)(a.batch * kt), use_part ? nsplit : 1);
+  cudaError_t e = cudaFuncSetAttribute(bwd_key64_tc_kernel<kDvOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64Smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(bwd_key64_tc_kernel<kDkOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64Smem);
+  if (e != cudaSuccess) return e;
+  bwd_key64_tc_kernel<kDvOnly><<<grid, 256, k64Smem, st>>>(p);
+  count_launch();
+  bwd_key64_tc_kernel<kDkOnly><<<grid, 256, k64Smem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }

@@ -200,11 +200,13 @@ def test_backward_mla_simt_forced():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("env", [{"LOZA_TEST_BACKWARD_KERNEL": "2"}, {"LOZA_TEST_BACKWARD_KERNEL": "3"}])
+@pytest.mark.parametrize("env", [{"LOZA_TEST_BACKWARD_KERNEL": "2"}, {"LOZA_TEST_BACKWARD_KERNEL": "3"},
+                                 {"LOZA_TEST_BACKWARD_KERNEL": "4"}])
 def test_backward_mma_paths_forced(env):
-    """The warp-level-MMA kernels of attn_bwd_mma.cu kept reachable through the MLA parity cases (test knob
-    backward, loza_debug_force_kernel): 2 = its key kernel and row kernel instead of the tcgen05 key kernel and
-    dS GEMM; 3 = tcgen05 key kernel, dQ by the row kernel instead of the tcgen05 dS GEMM."""
+    """The other key / dQ kernels kept reachable through the MLA parity cases (test knob backward,
+    loza_debug_force_kernel): 2 = the warp-MMA key kernel and row kernel of attn_bwd_mma.cu instead of the
+    tcgen05 key kernels and dS GEMM; 3 = tcgen05 key kernels, dQ by the row kernel instead of the tcgen05 dS
+    GEMM; 4 = the 32-key tcgen05 key kernel (dK and dV in one pass) instead of the 64-key dV / dK pair."""
     import os
     import subprocess
     import sys
