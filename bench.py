@@ -695,8 +695,8 @@ def decode_rows(args, peaks, flush):
                          "ssa_frac_hbm": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                          "ssa_bytes": by, "ssa_timing": f"CUDA graph of {R} steps, 4 rotating windows"}
     # decode sharded by heads (north star; SURVEY.md §8 e "if B < R"): one GPU's share of a head-sharded decode,
-    # B64 with H/2 = 32 heads over the same latent windows (the key-split pair kernel, attn_tc_decode_ks.cu);
-    # per-GPU bytes hardly drop (the window is shared by all heads)
+    # B64 with H/2 = 32 heads over the same latent windows (the pair-cooperative kernel with zero-padded heads,
+    # attn_tc_decode_coop.cu); per-GPU bytes hardly drop (the window is shared by all heads)
     if "131072" in res:
         ctx, Hs = 131072, 32
         qh = qd[:, :, :Hs].contiguous()
@@ -707,7 +707,7 @@ def decode_rows(args, peaks, flush):
         res["heads32_131072"] = {"ssa_us": ms * 1e3, "ssa_tokens_per_s": B / (ms * 1e-3),
                                  "ssa_gbs": by / (ms * 1e-3) / 1e9,
                                  "ssa_frac_hbm": by / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
-                                 "kernel": "key-split pair (attn_tc_decode_ks.cu)",
+                                 "kernel": "pair-cooperative, heads 32..63 zero-padded (attn_tc_decode_coop.cu)",
                                  "note": "B64, 32 of 64 heads: one GPU of a 2-way head-sharded decode"}
     # full-attention comparators after every SSA row (their long max-bandwidth runs heat the GPU and slowed
     # SSA rows timed right after them by up to 30%)

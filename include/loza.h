@@ -97,10 +97,10 @@ loza_status_t ssa_prefill(const loza_attn_args_t* args, loza_pattern_t pattern, 
  * kernels set it to LOZA_ERR_SHAPE when a seq_len was outside [1, T_cap] (they clamp it and continue); the
  * caller reads and resets it. The rest holds the flattened kernel's per-sequence counters (left at zero by
  * every call) and split partials.
- * bf16 path kernels: while 2*batch <= SM count, a CTA pair per sequence -- the pair-cooperative kernel for
- * H == 64 (attn_tc_decode_coop.cu), the key-split pair kernel for H < 64 (decode sharded by heads: every GPU
- * still reads the whole latent window; attn_tc_decode_ks.cu); otherwise (H == 64 only) a flattened split-KV
- * kernel. */
+ * bf16 path kernels: while 2*batch <= SM count, a CTA pair per sequence -- the pair-cooperative kernel
+ * (attn_tc_decode_coop.cu) for any H <= 64 (H < 64: decode sharded by heads; every GPU still reads the whole
+ * latent window, the missing heads are zero-padded); otherwise (H == 64 only) a flattened split-KV kernel.
+ * The key-split pair kernel (attn_tc_decode_ks.cu) is reachable through loza_debug_force_kernel. */
 loza_status_t ssa_decode(const loza_attn_args_t* args, const int32_t* seq_lens_dev,
                          loza_pattern_t pattern, void* ws, size_t ws_bytes, loza_stream_t stream);
 
@@ -290,7 +290,7 @@ const char* loza_last_error(void);           /* thread-local text of the last er
 uint64_t loza_kernel_launches(void);         /* number of library kernel launches so far (process) */
 int32_t loza_num_sms(void);                  /* SM count of the current device (0 if unknown) */
 /* Test hook: override the automatic kernel choice of a family, process-wide (the library never reads the
- * environment). "decode": 0 auto, 1 pair-cooperative (H == 64), 2 key-split pair; "backward": 0 auto, 1 FFMA
+ * environment). "decode": 0 auto, 1 pair-cooperative (H <= 64), 2 key-split pair; "backward": 0 auto, 1 FFMA
  * kernels, 2 warp-MMA key and row kernels, 3 tcgen05 key kernel + warp-MMA row kernel for dQ, 4 the 32-key
  * tcgen05 key kernel (dK and dV in one pass) instead of the 64-key dV / dK kernel pair. A forced
  * kernel that cannot take a problem falls back to the automatic choice. Returns 0, or -1 for an unknown

@@ -20,6 +20,9 @@
 //  * S runs two tiles ahead of PV (MMA order S(0), S(1), S(2), PV(0), S(3), PV(1), ..., three S^T buffers in
 //    TMEM) so the HBM-bound K rows of tile i + 2 are in flight while P(i) is being made; the softmax of tile i
 //    waits for PV(i - 2) before it rewrites that tile's P buffer and staging block.
+//  * H < 64 (a head-sharded GPU): the Q rows >= H are TMA zero-fill (the padded heads' columns are computed and
+//    dropped at the store); the work is that of H = 64, which is still faster than the key-split kernel
+//    (attn_tc_decode_ks.cu, now reachable through the test knob only): the window's bytes dominate.
 //  * Loads: warp 0 of each CTA (Q halves first through 9 chunk barriers; then a ring of 4 x 32 KB items in
 //    MMA order K(0), K(1), K(2), V(0), K(3), V(1), ...; pair TMA with completion on the leader's barriers);
 //    warp 1 of the leader issues every UMMA; warps 2-9 of both CTAs run the softmax.
@@ -89,7 +92,7 @@ constexpr uint32_t kPFullArrivals = kArrivalsPerPair + 2;  // + the transfer war
 struct CoopParams {
   CUtensorMap q_map, k_map, v_map;
   const int32_t* seq_lens;
-  int32_t batch, s, l, b;
+  int32_t batch, heads, s, l, b;  // heads <= 64: a head-sharded GPU's Q rows >= heads are TMA zero-fill
   int32_t ring;
   int64_t t_cap;
   int32_t n_rows;  // cache rows (an absent sub-block maps here: out of bounds, zero-filled)
@@ -277,7 +280,9 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       nr = nr > 128 ? 128 : nr;
       if (nr > 0) bulk_prefetch_l2(p.kraw + bi * p.k_sb_bytes + row * p.k_st_bytes, (uint32_t)(nr * p.k_st_bytes));
     }
-    if (p.qraw) bulk_prefetch_l2(p.qraw + bi * p.q_sb_bytes + rank * 32 * kDqk * 2, 32 * kDqk * 2);
+    const int nh = p.heads - 32 * (int)rank;  // this CTA's real Q rows
+    if (p.qraw && nh > 0)
+      bulk_prefetch_l2(p.qraw + bi * p.q_sb_bytes + rank * 32 * kDqk * 2, (uint32_t)((nh < 32 ? nh : 32) * kDqk * 2));
   }
 #endif
   asm volatile("griddepcontrol.wait;" ::: "memory");  // inputs of the previous kernel are visible from here
@@ -651,7 +656,8 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       const uint32_t h = 32 * ch + lane;
       invl[h] = 1.0f / lt;
       const float mh = m_mine;
-      if (p.lse && rank == 0) p.lse[(int64_t)bi * kH + h] = (mh * 0.69314718055994531f) + __logf(lt);
+      if (p.lse && rank == 0 && h < (uint32_t)p.heads)
+        p.lse[(int64_t)bi * p.heads + h] = (mh * 0.69314718055994531f) + __logf(lt);
     }
     mbar_wait(bar(kBarOFull + (gl & 1)), (gl >> 1) & 1);
     if (warp == 2) CTRACE(10, 1);
@@ -686,12 +692,13 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           const float r = __shfl_xor_sync(0xffffffffu, even ? c : a, 1);
           const uint32_t pk = even ? pack_bf16x2(a, r) : pack_bf16x2(r, c);
           const int h = 32 * (int)ch + j + (even ? 0 : 1);
-          asm volatile("st.global.b32 [%0], %1;" ::"l"(ob + (int64_t)h * p.o_sh), "r"(pk) : "memory");
+          if (h < p.heads) asm volatile("st.global.b32 [%0], %1;" ::"l"(ob + (int64_t)h * p.o_sh), "r"(pk) : "memory");
         }
       } else {
         float* ob = reinterpret_cast<float*>(p.o) + (int64_t)bi * p.o_sb + gd;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) ob[(int64_t)(32 * ch + j) * p.o_sh] = __uint_as_float(ov[j]) * w[j];
+        for (int j = 0; j < 32; ++j)
+          if ((int)(32 * ch) + j < p.heads) ob[(int64_t)(32 * ch + j) * p.o_sh] = __uint_as_float(ov[j]) * w[j];
       }
     }
     if (warp == 2) CTRACE(10, 2);
@@ -722,7 +729,7 @@ unsigned long long* g_pair_trace = nullptr;  // loza_debug_set_pair_trace
 int g_trace_cluster = 0;
 
 bool decode_coop_eligible(const AttnProblem& a, int sms) {
-  return a.sparse && a.heads == kH && a.d_qk == kDqk && a.d_v == kDv && a.b % 128 == 0 &&
+  return a.sparse && a.heads >= 1 && a.heads <= kH && a.d_qk == kDqk && a.d_v == kDv && a.b % 128 == 0 &&
          2 * (int64_t)a.batch <= sms && a.n_kv < (1ll << 31);
 }
 
@@ -742,12 +749,13 @@ bool decode_pair_dispatch(const AttnProblem& a, int32_t* status, cudaStream_t st
 }
 
 cudaError_t launch_decode_coop(const AttnProblem& a, int32_t* status, cudaStream_t st) {
-  if (a.heads != kH || a.d_qk != kDqk || a.d_v != kDv) return cudaErrorNotSupported;
+  if (a.heads < 1 || a.heads > kH || a.d_qk != kDqk || a.d_v != kDv) return cudaErrorNotSupported;
   if (a.n_kv >= (1ll << 31)) return cudaErrorNotSupported;
   CoopParams p;
   memset(&p, 0, sizeof(p));
   p.seq_lens = a.seq_lens;
   p.batch = a.batch;
+  p.heads = a.heads;
   p.s = a.s;
   p.l = a.l;
   p.b = a.b;
@@ -769,7 +777,7 @@ cudaError_t launch_decode_coop(const AttnProblem& a, int32_t* status, cudaStream
   p.trace_cluster = g_trace_cluster;
   p.status = status;
   const KvSeg& s = a.kv.seg[0];
-  if (!encode_3d(&p.q_map, a.q, kDqk, kH, a.batch, a.q_sh, a.q_sb, 32)) return cudaErrorInvalidValue;
+  if (!encode_3d(&p.q_map, a.q, kDqk, (uint64_t)a.heads, a.batch, a.q_sh, a.q_sb, 32)) return cudaErrorInvalidValue;
   if (!encode_3d(&p.k_map, s.k, kDqk, (uint64_t)a.n_kv, a.batch, s.k_st, s.k_sb, 128)) return cudaErrorInvalidValue;
   if (!encode_4d_chunks(&p.v_map, s.v, kDv, (uint64_t)a.n_kv, a.batch, s.v_st, s.v_sb, 32, 4))
     return cudaErrorInvalidValue;

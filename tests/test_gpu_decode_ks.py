@@ -1,8 +1,9 @@
-"""The key-split pair decode kernel (attn_tc_decode_ks.cu; SURVEY.md §8 a7 and e, decode sharded by heads).
+"""Head-sharded decode (SURVEY.md §8 a7 and e) and the key-split pair decode kernel (attn_tc_decode_ks.cu).
 
 - H < 64 (north star: decode "shards by batch and heads"): every GPU of a head-sharded decode runs
-  ssa_decode with its H/R heads over the same latent window. Against the fp64 oracle on ragged seq_lens, both
-  output dtypes, LSE, four patterns, and the bounded ring cache.
+  ssa_decode with its H/R heads over the same latent window (the pair-cooperative kernel with zero-padded
+  heads by default; the key-split kernel through test knob decode = 2). Against the fp64 oracle on ragged
+  seq_lens, both output dtypes, LSE, four patterns, and the bounded ring cache.
 - H == 64 through the same kernel (test knob decode = 2): the whole decode + ring parity suites re-run in a
   subprocess (the library never reads the environment; tests/conftest.py applies LOZA_TEST_DECODE_KERNEL).
 - The decode workspace's status word: a seq_len outside [1, n_kv] is reported (LOZA_ERR_SHAPE), the row is
@@ -107,5 +108,15 @@ def test_key_split_kernel_through_the_h64_parity_suites():
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_tc_decode.py"),
                         os.path.join(ROOT, "tests", "test_ring_cache.py")],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_key_split_kernel_head_sharded():
+    """The key-split kernel (test knob decode = 2) through the H < 64 parity cases above."""
+    env = dict(os.environ, LOZA_TEST_DECODE_KERNEL="2")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "-k", "head_sharded_vs_oracle or ring_head_sharded",
+                        os.path.join(ROOT, "tests", "test_gpu_decode_ks.py")],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
