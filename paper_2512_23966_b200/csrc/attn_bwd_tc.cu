@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
 // Q 4x + dO 4x (1112 KB), and every UMMA is M128 N64 (48 tensor cycles) instead of M128 N32.
 // TMEM: dV kernel dV^T 256 + S 2 x 64; dK kernel dK^T 320 + S 64 + dP 64 (single-buffered: the P/dS warps
 // release them right after their TMEM loads). SMEM: ring 4 x 32 KB, K tile 72 KB, P or dS 16 KB (SW128).
-constexpr int kDvOnly = 1, kDkOnly = 2;
+constexpr int kDvOnly = 1, kDkOnly = 2, kDkFromP = 3;
 constexpr int k64Keys = 64;
 constexpr int k64Stages = 4;
 constexpr int k64KBytes = 9 * k64Keys * 128;       // 72 KB: [9 chunks][64 keys][64]
@@ -436,12 +436,17 @@ constexpr int k64OffTmemPtr = k64OffBar + 8 * k64NumBars;
 constexpr int k64Smem = k64OffTmemPtr + 16 + 1024;
 static_assert(k64Smem <= 232448, "smem");
 
+// MODE kDkFromP (SSA, with the dS row buffer): the dV kernel has left P (bf16) in the dS rows' slots, so the dK
+// kernel reads P there instead of recomputing S: its first pass is dP = dO V^T only (dP double-buffered in
+// TMEM), and it overwrites each slot with dS = P (dP - D). Per 128-row tile it moves dO + Q + 16 KB of P.
 template <int MODE>
 __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_constant__ TcBwdParams p) {
   constexpr bool kIsDv = MODE == kDvOnly;
-  constexpr int kSBufs = kIsDv ? 2 : 1;  // S (and dP) buffers in TMEM
-  constexpr uint32_t kTmemAcc = 0;                     // dV^T: 4 x 64 columns, dK^T: 5 x 64
-  constexpr uint32_t kTmemS = kIsDv ? 256 : 320, kTmemDP = 384;
+  constexpr bool kFromP = MODE == kDkFromP;
+  constexpr int kSBufs = kIsDv || kFromP ? 2 : 1;  // S (and / or dP) buffers in TMEM
+  constexpr uint32_t kTmemAcc = 0;                  // dV^T: 4 x 64 columns, dK^T: 5 x 64
+  constexpr uint32_t kTmemS = kIsDv ? 256 : 320, kTmemDP = kFromP ? 320 : 384;
+  constexpr uint32_t kDPStride = kFromP ? 64 : 0;   // dP buffer stride (double-buffered when S is not computed)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t sbase = (sraw + 1023u) & ~1023u;
@@ -532,7 +537,8 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
       };
       // the UMMA issuer's order: the first pass (S, and dP) of tile t + 1 before the gradient pass of tile t
       auto load_first = [&](int rb) {
-        for (int q = 0; q < kQPairs; ++q) load_pair(&p.q_map, q, rb);
+        if (!kFromP)
+          for (int q = 0; q < kQPairs; ++q) load_pair(&p.q_map, q, rb);
         if (!kIsDv)
           for (int q = 0; q < kOPairs; ++q) load_pair(&p.o_map, q, rb);
       };
@@ -579,7 +585,7 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
         mbar_wait(bar(k64BarSFree + buf), (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t tS = tmem + kTmemS + 64 * buf;
-        for (int q = 0; q < kQPairs; ++q) {  // S = Q K^T
+        for (int q = 0; q < (kFromP ? 0 : kQPairs); ++q) {  // S = Q K^T
           take();
           if (elect_one()) {
             const int nk = q < kQPairs - 1 ? 8 : 4;
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
             if (elect_one()) {
               for (int k = 0; k < 8; ++k) {
                 const uint32_t ch = 2 * q + (k >> 2), kk = k & 3;
-                umma_bf16_1sm(tmem + kTmemDP,
+                umma_bf16_1sm(tmem + kTmemDP + kDPStride * buf,
                               sdesc_sw128(sbase + k64OffRing + slot * kPairBytes + (k >> 2) * 16384 + 32 * kk, 16, 1024),
                               sdesc_sw128(sbase + k64OffK + ch * (k64Keys * 128) + 32 * kk, 16, 1024), id_s,
                               (q | k) != 0);
@@ -655,14 +661,34 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
       const float lse2 = rv ? p.lse[((int64_t)bi * H + h) * p.n_q + t] * kLog2e : 0.f;
       const float Dr = (!kIsDv && rv) ? p.D[(int64_t)bi * rows + rr] : 0.f;
       const bool win = jsink || kb >= pos / p.b - p.l + 1;
+      // this row's slots of block kb in the dS row buffer (P from the dV kernel, then dS)
+      uint4* dsrow = nullptr;
+      if (p.ds && rv) {
+        int lbq = pos / p.b - p.l + 1;
+        if (lbq < p.s) lbq = p.s;
+        const int W = (p.s + p.l) * p.b;
+        const int slot = kb < p.s ? j0 : p.s * p.b + (kb - lbq) * p.b + (j0 - kb * p.b);
+        dsrow = reinterpret_cast<uint4*>(p.ds + ((int64_t)bi * rows + rr) * W + slot);
+      }
+      uint32_t pin[32];  // kFromP: P (bf16 pairs), loaded before the dP wait
+      if (kFromP) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint4 x = dsrow ? dsrow[u] : make_uint4(0, 0, 0, 0);
+          pin[4 * u] = x.x;
+          pin[4 * u + 1] = x.y;
+          pin[4 * u + 2] = x.z;
+          pin[4 * u + 3] = x.w;
+        }
+      }
       mbar_wait(bar(k64BarSFull + buf), use & 1);
       tc_fence_after();
       uint32_t pk[32];
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {  // keys 32 hf .. 32 hf + 31
         uint32_t sv[32], dv[32];
-        tmem_ld32(tl + kTmemS + 64 * buf + 32 * hf, sv);
-        if (!kIsDv) tmem_ld32(tl + kTmemDP + 32 * hf, dv);
+        if (!kFromP) tmem_ld32(tl + kTmemS + 64 * buf + 32 * hf, sv);
+        if (!kIsDv) tmem_ld32(tl + kTmemDP + kDPStride * buf + 32 * hf, dv);
         tmem_wait_ld();
         if (hf == 1) {
           tc_fence_before();
@@ -676,20 +702,21 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
           for (int e = 0; e < 2; ++e) {
             const int j = j0 + 32 * hf + c + e;
             const bool ok = rv && win && j < p.n_kv && (!p.causal || j <= pos);
-            const float pv = ok ? ex2(fmaf(__uint_as_float(sv[c + e]), p.sl2, -lse2)) : 0.f;
+            float pv;
+            if (kFromP) {
+              const uint32_t w2 = pin[16 * hf + (c >> 1)];
+              pv = e ? __uint_as_float(w2 & 0xFFFF0000u) : __uint_as_float(w2 << 16);
+            } else {
+              pv = ok ? ex2(fmaf(__uint_as_float(sv[c + e]), p.sl2, -lse2)) : 0.f;
+            }
             v2[e] = kIsDv ? pv : pv * (__uint_as_float(dv[c + e]) - Dr);
           }
           pk[16 * hf + (c >> 1)] = pack_bf16x2(v2[0], v2[1]);
         }
       }
-      if (!kIsDv && p.ds && rv) {  // this row's 64 dS values at its slots of block kb
-        int lbq = pos / p.b - p.l + 1;
-        if (lbq < p.s) lbq = p.s;
-        const int W = (p.s + p.l) * p.b;
-        const int slot = kb < p.s ? j0 : p.s * p.b + (kb - lbq) * p.b + (j0 - kb * p.b);
-        uint4* dst = reinterpret_cast<uint4*>(p.ds + ((int64_t)bi * rows + rr) * W + slot);
+      if (dsrow) {  // this row's 64 values at its slots of block kb: P (dV kernel), dS (dK kernels)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        for (int u = 0; u < 8; ++u) dsrow[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       }
       mbar_wait(bar(k64BarPFree), (tc & 1) ^ 1);
       // row of 128 B = 8 x 16-B units, SWIZZLE_128B: unit u at (u ^ row & 7)
@@ -1053,10 +1080,16 @@ cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* d
   cudaError_t e = cudaFuncSetAttribute(bwd_key64_tc_kernel<kDvOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64Smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(bwd_key64_tc_kernel<kDkOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64Smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(bwd_key64_tc_kernel<kDkFromP>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64Smem);
   if (e != cudaSuccess) return e;
+  // with the dS row buffer (SSA): the dV kernel leaves P there and the dK kernel reads it (no S recompute)
   bwd_key64_tc_kernel<kDvOnly><<<grid, 256, k64Smem, st>>>(p);
   count_launch();
-  bwd_key64_tc_kernel<kDkOnly><<<grid, 256, k64Smem, st>>>(p);
+  if (ds)
+    bwd_key64_tc_kernel<kDkFromP><<<grid, 256, k64Smem, st>>>(p);
+  else
+    bwd_key64_tc_kernel<kDkOnly><<<grid, 256, k64Smem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }
