@@ -632,6 +632,31 @@ int sink_tiles(const AttnProblem& a) {
 
 }  // namespace
 
+// per-device side stream + fork / join events of the backward (D beside the dV kernel); per host thread
+struct SideCtx {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+cudaError_t side_ctx(SideCtx** out) {
+  static thread_local SideCtx ctx[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  SideCtx& c = ctx[dev];
+  if (!c.side) {
+    e = cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      c.side = nullptr;
+      return e;
+    }
+  }
+  *out = &c;
+  return cudaSuccess;
+}
+
 size_t backward_mma_part_bytes(const AttnProblem& a) {
   if (!a.sparse || sink_splits(a) <= 1) return 0;
   return sizeof(float) * (size_t)a.batch * sink_tiles(a) * sink_splits(a) * kKKeys * kDKV;
@@ -698,9 +723,20 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
   // test knob backward = 4 keeps the 32-key kernel that accumulates dK and dV in one pass
   const bool key64 = knob(kKnobBackward) != 4 && backward_key64_eligible(a);
   if (tc_keys && !force_dq_mma && ds && backward_ds_eligible(a) && rows > 0 && a.n_kv > 0) {
-    if ((e = launch_bwd_D(a, dout, D, st)) != cudaSuccess) return e;
-    e = key64 ? launch_bwd_key64_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st)
-              : launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st);
+    if (key64) {
+      // D = rowsum(dO O) on a side stream, beside the dV kernel (which does not read it; its CTAs leave room
+      // for D's), joined before the dK kernel
+      SideCtx* sc = nullptr;
+      if ((e = side_ctx(&sc)) != cudaSuccess) return e;
+      if ((e = cudaEventRecord(sc->fork, st)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(sc->side, sc->fork, 0)) != cudaSuccess) return e;
+      if ((e = launch_bwd_D(a, dout, D, sc->side)) != cudaSuccess) return e;
+      if ((e = cudaEventRecord(sc->join, sc->side)) != cudaSuccess) return e;
+      e = launch_bwd_key64_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st, sc->join);
+    } else {
+      if ((e = launch_bwd_D(a, dout, D, st)) != cudaSuccess) return e;
+      e = launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st);
+    }
     if (e != cudaSuccess) return e;
     if ((e = launch_bwd_dq_tc(a, ds, dq, st)) != cudaSuccess) return e;
     if (use_part) {

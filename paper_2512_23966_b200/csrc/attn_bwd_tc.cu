@@ -1040,7 +1040,8 @@ cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk
 bool backward_key64_eligible(const AttnProblem& a) { return !a.sparse || a.b % k64Keys == 0; }
 
 cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
-                                float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st) {
+                                float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st,
+                                cudaEvent_t d_ready) {
   TcBwdParams p;
   const auto& kv = a.kv.seg[0];
   const uint64_t rows = (uint64_t)a.n_q * a.heads;
@@ -1086,6 +1087,7 @@ cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* d
   // with the dS row buffer (SSA): the dV kernel leaves P there and the dK kernel reads it (no S recompute)
   bwd_key64_tc_kernel<kDvOnly><<<grid, 256, k64Smem, st>>>(p);
   count_launch();
+  if (d_ready && (e = cudaStreamWaitEvent(st, d_ready, 0)) != cudaSuccess) return e;  // D (side stream) for dS
   if (ds)
     bwd_key64_tc_kernel<kDkFromP><<<grid, 256, k64Smem, st>>>(p);
   else
