@@ -23,6 +23,8 @@
 //  * H < 64 (a head-sharded GPU): the Q rows >= H are TMA zero-fill (the padded heads' columns are computed and
 //    dropped at the store); the work is that of H = 64, which is still faster than the key-split kernel
 //    (attn_tc_decode_ks.cu, now reachable through the test knob only): the window's bytes dominate.
+//  * Up to 10 helper clusters on the SMs the pairs leave idle L2-prefetch the later pair tiles' cache rows (paced
+//    by the global timer), so the pairs' TMA loads of those tiles mostly hit L2.
 //  * Loads: warp 0 of each CTA (Q halves first through 9 chunk barriers; then a ring of 4 x 32 KB items in
 //    MMA order K(0), K(1), K(2), V(0), K(3), V(1), ...; pair TMA with completion on the leader's barriers);
 //    warp 1 of the leader issues every UMMA; warps 2-9 of both CTAs run the softmax.
@@ -36,6 +38,15 @@
 #ifndef DECODE_EARLY_PF
 #define DECODE_EARLY_PF 1
 #endif
+// Helper clusters on the SMs the pairs leave idle (B < SMs / 2): they L2-prefetch every sequence's cache rows of
+// pair tiles 1, 2, ... (tile t issued (t - 1) x kHelperDelta ns after the dependency wait). Measured (B64 at 128K,
+// bench timing, one box): no helpers 22.4 us; 10 helper clusters 21.2 us for any pacing 0-3.5 us; the same
+// clusters idle 22.85; prefetching tile 1 only 23.1, tiles 2.. only 23.5, tiles 0.. 23.4; 5 clusters 29.5.
+#ifndef DECODE_HELPER_CLUSTERS
+#define DECODE_HELPER_CLUSTERS 10
+#endif
+constexpr int kHelperClusters = DECODE_HELPER_CLUSTERS;
+constexpr unsigned long long kHelperDelta = 2000;
 
 namespace loza {
 
@@ -223,6 +234,39 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
   float* invl = reinterpret_cast<float*>(smem + kOffInv);
   const uint32_t rank = cluster_ctarank(), partner = rank ^ 1;
   const int bi = (int)(blockIdx.x >> 1);
+  if (bi >= p.batch) {  // helper cluster (idle SMs): L2 prefetch of the sequences' later pair tiles, paced
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x >= 32 || !p.kraw) return;
+    const int hid = (int)blockIdx.x - 2 * p.batch, nh = (int)gridDim.x - 2 * p.batch;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int t = 1;; ++t) {
+      {
+        unsigned long long g;
+        do {
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        } while (g < t0 + (unsigned long long)(t - 1) * kHelperDelta);
+      }
+      bool any = false;
+      for (int sq = hid; sq < p.batch; sq += nh) {
+        const SeqTiles sqt = seq_tiles(p, sq);
+        if (2 * t >= sqt.n_tiles) continue;
+        any = true;
+        if (lane < 2) {
+          const int32_t k0 = sub_k0(sqt, 2 * t + (int)lane);
+          if (k0 >= 0) {
+            const int32_t row = kv_row(p, k0);
+            int32_t nr = p.n_rows - row;
+            nr = nr > 128 ? 128 : nr;
+            if (nr > 0) bulk_prefetch_l2(p.kraw + sq * p.k_sb_bytes + row * p.k_st_bytes, (uint32_t)(nr * p.k_st_bytes));
+          }
+        }
+      }
+      if (!__any_sync(0xffffffffu, any)) break;
+    }
+    return;
+  }
 
   if (p.trace && threadIdx.x == 0) {  // per-CTA wall-clock span (globaltimer ns) after the timeline slots
     unsigned long long g;
@@ -785,7 +829,12 @@ cudaError_t launch_decode_coop(const AttnProblem& a, int32_t* status, cudaStream
   cudaError_t ea = cudaFuncSetAttribute(decode_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
   if (ea != cudaSuccess) return ea;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(2 * a.batch));
+  int nclusters = a.batch;
+  if (p.kraw) {  // helper clusters on the SMs the pairs leave idle (contiguous cache rows only)
+    const int spare = (device_sm_count() - 2 * a.batch) / 2;
+    nclusters += spare > 0 ? (spare < kHelperClusters ? spare : kHelperClusters) : 0;
+  }
+  cfg.gridDim = dim3((unsigned)(2 * nclusters));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemAlloc;
   cfg.stream = st;
