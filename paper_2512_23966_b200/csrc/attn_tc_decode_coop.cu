@@ -72,7 +72,7 @@ constexpr int kBarEmpty = kBarFull + kStages;
 constexpr int kBarQFull = kBarEmpty + kStages;    // [9]
 // S runs kAhead tiles ahead of PV. Measured (B64 at 128K, bench timing): 1 (FA order) 22.2 us, 2 21.1-21.2,
 // 3 21.85, 4 21.98 -- beyond 2 the V re-reads bunch up behind the last K tile
-constexpr int kAhead = 2;
+constexpr int kAhead = 2;  // with the helper clusters: 1 21.8 us, 2 21.3, 3 22.4
 constexpr int kSBufs = kAhead + 1;                // S^T buffers in TMEM
 constexpr int kBarSFull = kBarQFull + kChunks;    // [kSBufs]
 constexpr int kBarSFree = kBarSFull + kSBufs;     // [kSBufs]
