@@ -707,6 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     if (warp == 2) CTRACE(10, 1);
     tc_fence_after();
     named_bar_sync(1, kSmThreads);  // invl written
+    if (warp == 2) CTRACE(10, 3);
     float w[32];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -724,20 +725,27 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     tmem_ld32(taddr + kTmemO + 32 * ch, ovg[0]);
     tmem_ld32(taddr + kTmemO + 64 + 32 * ch, ovg[1]);
     tmem_wait_ld();
+    if (warp == 2) CTRACE(10, 6);
 #pragma unroll
     for (int g = 0; g < 2; ++g) {
+      if (g == 1 && warp == 2) CTRACE(10, 7);
       const uint32_t(&ov)[32] = ovg[g];
       const int gd = 256 * (int)rank + 128 * g + (int)t;  // output dim
       if (p.out_bf16) {
-        uint16_t* ob = reinterpret_cast<uint16_t*>(p.o) + (int64_t)bi * p.o_sb + (even ? gd : gd - 1);
+        uint16_t* ob = reinterpret_cast<uint16_t*>(p.o) + (int64_t)bi * p.o_sb + (even ? gd : gd - 1) +
+                       (int64_t)(32 * (int)ch + (even ? 0 : 1)) * p.o_sh;
+        // all 16 swaps first (independent shuffles pipeline), then the 16 stores
+        uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
           const float a = __uint_as_float(ov[j]) * w[j], c = __uint_as_float(ov[j + 1]) * w[j + 1];
           const float r = __shfl_xor_sync(0xffffffffu, even ? c : a, 1);
-          const uint32_t pk = even ? pack_bf16x2(a, r) : pack_bf16x2(r, c);
-          const int h = 32 * (int)ch + j + (even ? 0 : 1);
-          if (h < p.heads) asm volatile("st.global.b32 [%0], %1;" ::"l"(ob + (int64_t)h * p.o_sh), "r"(pk) : "memory");
+          pk[j >> 1] = even ? pack_bf16x2(a, r) : pack_bf16x2(r, c);
         }
+        const int h0 = 32 * (int)ch + (even ? 0 : 1);
+#pragma unroll
+        for (int j = 0; j < 32; j += 2)
+          if (h0 + j < p.heads) *reinterpret_cast<uint32_t*>(ob + (int64_t)j * p.o_sh) = pk[j >> 1];
       } else {
         float* ob = reinterpret_cast<float*>(p.o) + (int64_t)bi * p.o_sb + gd;
 #pragma unroll

@@ -69,4 +69,4 @@ for i in (R // 2, R - 1):
         base = t[0, 0, 0]
         print(f"  CTA {r}")
         for s, nm in enumerate(names):
-            print(f"  {nm:>10s} " + " ".join(f"{(x - base) if x > 0 else -1:7d}" for x in t[s, r, :6]))
+            print(f"  {nm:>10s} " + " ".join(f"{(x - base) if x > 0 else -1:7d}" for x in t[s, r, :(8 if nm == 'end' else 6)]))
