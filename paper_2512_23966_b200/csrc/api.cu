@@ -102,6 +102,9 @@ loza_status_t choose_path(const loza_attn_args_t* a, const AttnProblem& p, Path*
       (a->v_stride_b * esz) % 16 || (a->q_stride_b * esz) % 16 || (a->q_stride_tok * esz) % 16 ||
       (a->q_stride_head * esz) % 16)
     return fail(LOZA_ERR_SHAPE, "bf16 path needs 16-byte aligned strides");
+  if (a->out_dtype == LOZA_BF16 &&
+      ((a->o_stride_b * esz) % 16 || (a->o_stride_tok * esz) % 16 || (a->o_stride_head * esz) % 16))
+    return fail(LOZA_ERR_SHAPE, "bf16 output needs 16-byte aligned strides (16-byte / TMA stores)");
   if (!p.seq_lens) {
     if (a->q_stride_head != a->d_qk || a->q_stride_tok != (int64_t)a->heads * a->d_qk)
       return fail(LOZA_ERR_UNSUPPORTED, "bf16 prefill needs head-contiguous q rows");
