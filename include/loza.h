@@ -292,7 +292,8 @@ int32_t loza_num_sms(void);                  /* SM count of the current device (
 /* Test hook: override the automatic kernel choice of a family, process-wide (the library never reads the
  * environment). "decode": 0 auto, 1 pair-cooperative (H <= 64), 2 key-split pair; "backward": 0 auto, 1 FFMA
  * kernels, 2 warp-MMA key and row kernels, 3 tcgen05 key kernel + warp-MMA row kernel for dQ, 4 the 32-key
- * tcgen05 key kernel (dK and dV in one pass) instead of the 64-key dV / dK kernel pair. A forced
+ * tcgen05 key kernel (dK and dV in one pass) instead of the 64-key dV / dK kernel pair, 5 the 64-key dV / dK
+ * kernels instead of the 128-key CTA-pair kernels (SSA with b = 128). A forced
  * kernel that cannot take a problem falls back to the automatic choice. Returns 0, or -1 for an unknown
  * family / variant. */
 int32_t loza_debug_force_kernel(const char* family, int32_t variant);

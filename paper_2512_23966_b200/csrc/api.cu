@@ -376,7 +376,7 @@ int32_t loza_debug_force_kernel(const char* family, int32_t variant) {
     g_knobs[kKnobDecode].store(variant);
     return 0;
   }
-  if (strcmp(family, "backward") == 0 && variant >= 0 && variant <= 4) {
+  if (strcmp(family, "backward") == 0 && variant >= 0 && variant <= 5) {
     g_knobs[kKnobBackward].store(variant);
     return 0;
   }

@@ -719,8 +719,9 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
   const bool force_mma = knob(kKnobBackward) == 2;
   const bool force_dq_mma = knob(kKnobBackward) == 3;
   const bool tc_keys = !force_mma && backward_tc_eligible(a, dout);
-  // 64-key tiles (a dV kernel and a dK kernel, attn_bwd_tc.cu) unless the tile would straddle a block or the
-  // test knob backward = 4 keeps the 32-key kernel that accumulates dK and dV in one pass
+  // 64-key tiles (a dV kernel and a dK kernel, attn_bwd_tc.cu; 128-key CTA-pair kernels for SSA with b = 128
+  // unless the test knob backward = 5) unless the tile would straddle a block or the test knob backward = 4
+  // keeps the 32-key kernel that accumulates dK and dV in one pass
   const bool key64 = knob(kKnobBackward) != 4 && backward_key64_eligible(a);
   if (tc_keys && !force_dq_mma && ds && backward_ds_eligible(a) && rows > 0 && a.n_kv > 0) {
     if (key64) {
@@ -732,7 +733,8 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
       if ((e = cudaStreamWaitEvent(sc->side, sc->fork, 0)) != cudaSuccess) return e;
       if ((e = launch_bwd_D(a, dout, D, sc->side)) != cudaSuccess) return e;
       if ((e = cudaEventRecord(sc->join, sc->side)) != cudaSuccess) return e;
-      e = launch_bwd_key64_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st, sc->join);
+      e = launch_bwd_key64_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st, sc->join,
+                              knob(kKnobBackward) != 5);
     } else {
       if ((e = launch_bwd_D(a, dout, D, st)) != cudaSuccess) return e;
       e = launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st);

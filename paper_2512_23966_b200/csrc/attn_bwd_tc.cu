@@ -60,6 +60,8 @@ struct TcBwdParams {
   int32_t sparse, causal, s, l, b;
   int32_t nsplit, n_sink;
   uint32_t h_m, h_p;
+  unsigned long long* trace;  // debug timeline of pair cluster trace_cluster (pair kernels; NULL in production)
+  int32_t trace_cluster;
 };
 
 __device__ __forceinline__ int div_h(const TcBwdParams& p, int n) {
@@ -81,15 +83,23 @@ __device__ __forceinline__ void st_shared_v4(uint32_t a, uint32_t x, uint32_t y,
 // The CTA's row tiles (all roles walk the same sequence): segments as in attn_bwd_mma.cu's key kernel.
 struct RowIter {
   int L, m0, m1, p0, p1, R0, R1, qs, H, b;
-  int sig, rb, re;
+  int step = kRows;  // rows per tile
+  int sig, m, rb, re;
+  // L == 1: the row range [R0, R1) in order. L > 1: the query blocks m0 .. m1 in the order (m mod L, m), so at
+  // step sig every CTA of the grid streams blocks m = sig (mod L) and the CTAs that share a block read it together
   __device__ void next_seg() {
-    while (++sig < L) {
+    for (;;) {
       if (L == 1) {
+        if (++sig >= 1) return;
         rb = R0;
         re = R1;
       } else {
-        const int m = m0 + ((sig - m0) % L + L) % L;
-        if (m > m1) continue;
+        m += L;
+        if (sig < 0 || m > m1) {
+          if (++sig >= L) return;
+          m = m0 + ((sig - m0) % L + L) % L;
+          if (m > m1) continue;
+        }
         const int a = m * b > p0 ? m * b : p0, e = (m + 1) * b < p1 ? (m + 1) * b : p1;
         rb = (a - qs) * H;
         re = (e - qs) * H;
@@ -99,12 +109,13 @@ struct RowIter {
   }
   __device__ void start() {
     sig = -1;
+    m = 0;
     rb = re = 0;
     next_seg();
   }
   __device__ bool valid() const { return sig < L; }
   __device__ void advance() {
-    rb += kRows;
+    rb += step;
     if (rb >= re) next_seg();
   }
 };
@@ -133,15 +144,24 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
   }
   const bool split = p.sparse && kb < p.s && p.nsplit > 1;
   if (split) {
-    const int chunk = ((R1 - R0 + p.nsplit - 1) / p.nsplit + kRows - 1) / kRows * kRows;
-    const int a = R0 + (int)blockIdx.y * chunk, e = a + chunk;
-    R0 = a < R1 ? a : R1;
-    R1 = e < R1 ? e : R1;
+    // a sink tile's rows split by whole query blocks, each split walked in the local tiles' rotation (its reads
+    // hit the rows the local tiles stream at the same step)
+    if (p1 > p0) {
+      const int ma = p0 / p.b, nb = (p1 - 1) / p.b - ma + 1, cb = (nb + p.nsplit - 1) / p.nsplit;
+      const int a = (ma + (int)blockIdx.y * cb) * p.b, e = a + cb * p.b;
+      if (a > p0) p0 = a;
+      if (e < p1) p1 = e;
+    }
+    R0 = R1 = 0;
+    if (p1 > p0) {
+      R0 = (p0 - p.q_start) * H;
+      R1 = (p1 - p.q_start) * H;
+    }
   } else if (blockIdx.y > 0) {
     return;
   }
   RowIter it;
-  it.L = p.sparse && !split && kb >= p.s ? p.l : 1;
+  it.L = p.sparse && (split || kb >= p.s) ? p.l : 1;
   it.m0 = p0 / p.b;
   it.m1 = (p1 - 1) / p.b;
   it.p0 = p0;
@@ -470,15 +490,24 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
   }
   const bool split = p.sparse && kb < p.s && p.nsplit > 1;
   if (split) {
-    const int chunk = ((R1 - R0 + p.nsplit - 1) / p.nsplit + kRows - 1) / kRows * kRows;
-    const int a = R0 + (int)blockIdx.y * chunk, e = a + chunk;
-    R0 = a < R1 ? a : R1;
-    R1 = e < R1 ? e : R1;
+    // a sink tile's rows split by whole query blocks, each split walked in the local tiles' rotation (its reads
+    // hit the rows the local tiles stream at the same step)
+    if (p1 > p0) {
+      const int ma = p0 / p.b, nb = (p1 - 1) / p.b - ma + 1, cb = (nb + p.nsplit - 1) / p.nsplit;
+      const int a = (ma + (int)blockIdx.y * cb) * p.b, e = a + cb * p.b;
+      if (a > p0) p0 = a;
+      if (e < p1) p1 = e;
+    }
+    R0 = R1 = 0;
+    if (p1 > p0) {
+      R0 = (p0 - p.q_start) * H;
+      R1 = (p1 - p.q_start) * H;
+    }
   } else if (blockIdx.y > 0) {
     return;
   }
   RowIter it;
-  it.L = p.sparse && !split && kb >= p.s ? p.l : 1;
+  it.L = p.sparse && (split || kb >= p.s) ? p.l : 1;
   it.m0 = p0 / p.b;
   it.m1 = (p1 - 1) / p.b;
   it.p0 = p0;
@@ -773,6 +802,459 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
   }
 }
 
+// ------------------------------------------------------------------------ key side, 128-key pair tiles
+// The 64-key kernels above move every 128-row tile of Q and dO through one SM per 64 keys (288 KB per tile
+// for the dV kernel) and run M128 N64 UMMAs (48 cycles, smem-operand bound). Here a CTA pair (cta_group::2)
+// owns the 128 keys of one b-block (b = 128) and streams 256-row tiles, CTA r staging 64 keys (the N half of
+// every B operand) and half of each tile's operands:
+//   dV pair kernel (MODE kPairDv):
+//     S   [256 rows x 128 keys] = Q K^T    M256 N128 (A = CTA r's 128 rows of Q, B = its 64 keys): CTA r's TMEM
+//                                           holds S of its rows for all 128 keys
+//     P   = exp2(S scale log2e - LSE log2e) by 8 warps per CTA (thread = row, 64 keys); the P of CTA c's keys
+//           must end up in CTA c (the N half of the next B operand): the own half is written in place, the
+//           other half staged and moved by one 16 KB bulk DSMEM copy. The row's values also go to the dS row
+//           buffer (the dK kernel reads P there).
+//     dV^T [512 x 128] += dO^T P           M256 N128 per 256-dim group (A = dO^T MN-major: CTA r stages dims
+//                                           256 g + 128 r .. + 127 of all 256 rows)
+//   dK pair kernel (MODE kPairDk, SSA):
+//     dP  = dO V^T                          M256 N128 (A = CTA r's 128 rows of dO, B = V of its 64 keys)
+//     dS  = P (dP - D) (P read back from the dS row buffer), into the dS row buffer and, split by keys as above,
+//           into the two CTAs' dS buffers
+//     dK^T [576 x 128] += Q^T dS            three M256 N128 groups (dims 512.. of the third: CTA 0 stages
+//                                           chunk 8 and a zero-filled chunk 9, CTA 1 two zero-filled chunks)
+// Per SM and 128 x 128 (row, key) pairs the dV kernel moves 288 KB (the 64-key kernel: 576 KB) and the dK kernel
+// 320 KB (64-key: 588 KB), and every UMMA is M256 N128 (64 cycles for 2 x 128 x 128 x 16 MACs).
+// TMEM per CTA: dV kernel S 2 x 128 + dV^T 2 x 128 columns; dK kernel dK^T 3 x 128 + dP 128 (single-buffered:
+// the dS warps release it right after their TMEM loads). SMEM: ring 3 x 32 KB, K tile 72 KB (dV: 9 chunks) or
+// 64 KB (dK: V's 8), P / dS 32 KB, staging 16 KB. Warps 0-7 P / dS and the epilogue (warp w: TMEM lane quarter
+// w % 4, key half w / 4), warp 8 TMA, warp 9 UMMA issue (leader) and TMEM allocation, warp 10 the DSMEM copy.
+constexpr int kPairDv = 1, kPairDk = 2;
+constexpr int kPKeys = 128, kPRows = 2 * kRows;  // keys per pair tile, rows per pair row tile
+constexpr int kPThreads = 352, kPProd = 8, kPMma = 9, kPXfer = 10;
+template <int MODE>
+struct PairCfg {
+  static constexpr bool kDv = MODE == kPairDv;
+  static constexpr int kStages = 3;
+  static constexpr int kKChunks = kDv ? 9 : 8;             // the K tile (S needs 576 dims, dP only V's 512)
+  static constexpr int kKBytes = kKChunks * 64 * 128;      // [chunks][64 keys][64 dims]
+  static constexpr int kPBytes = kPRows * 128;             // P / dS: [256 rows][64 keys] bf16, SW128
+  static constexpr int kStBytes = kRows * 128;             // staging: [128 rows][the partner's 64 keys]
+  static constexpr int kOffRing = 0, kOffK = kStages * kPairBytes, kOffP = kOffK + kKBytes, kOffSt = kOffP + kPBytes,
+                       kOffBar = kOffSt + kStBytes;
+  static constexpr int kBarFull = 0, kBarEmpty = kStages, kBarK = 2 * kStages, kBarSFull = kBarK + 1,
+                       kBarSFree = kBarSFull + 2, kBarPLocal = kBarSFree + 2, kBarPStaged = kBarPLocal + 1,
+                       kBarPRecv = kBarPStaged + 1, kBarPFull = kBarPRecv + 1, kBarPFree = kBarPFull + 1,
+                       kBarAcc = kBarPFree + 1, kNumBars = kBarAcc + 1;
+  static constexpr int kOffTmemPtr = kOffBar + 8 * kNumBars;
+  static constexpr int kSmem = kOffTmemPtr + 16 + 1024;
+  static constexpr int kFirstItems = kDv ? kQPairs : kOPairs;  // Q (S) or dO (dP) of this CTA's 128 rows
+  static constexpr int kGroups = kDv ? 2 : 3;                  // 256-dim M groups of dV^T / dK^T
+  static constexpr uint32_t kTmemS = kDv ? 0 : 384, kTmemAcc = kDv ? 256 : 0;
+  static constexpr int kSBufs = kDv ? 2 : 1;
+};
+static_assert(PairCfg<kPairDv>::kSmem <= 232448 && PairCfg<kPairDk>::kSmem <= 232448, "smem");
+
+// clock64 timeline: trace[(slot * 2 + rank) * 64 + tile] for tiles < 64 of pair cluster trace_cluster
+#define BTRACE(slot, idx)                                                                                   \
+  do {                                                                                                      \
+    if (p.trace && pc == p.trace_cluster && blockIdx.y == 0 && (idx) < 64 && (threadIdx.x & 31) == 0)       \
+      p.trace[((slot) * 2 + rank) * 64 + (idx)] = clock64();                                                \
+  } while (0)
+
+template <int MODE>
+__global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
+    bwd_pair_tc_kernel(const __grid_constant__ TcBwdParams p) {
+  using C = PairCfg<MODE>;
+  constexpr bool kDvK = C::kDv;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sbase - sraw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank(), partner = rank ^ 1u;
+  const int H = p.heads;
+  const int ktiles = (p.n_kv + kPKeys - 1) / kPKeys;
+  const int pc = (int)(blockIdx.x >> 1);
+  const int bi = pc / ktiles, tile = pc - bi * ktiles, j0 = tile * kPKeys;
+  // rows attending keys [j0, j0 + 128) (b == 128: the tile is one block)
+  int p0 = p.causal ? j0 : 0, p1 = p.q_start + p.n_q;
+  const int kb = j0 / p.b;
+  if (p.sparse && kb >= p.s) {
+    const int pe = (kb + p.l) * p.b;
+    if (pe < p1) p1 = pe;
+  }
+  if (p0 < p.q_start) p0 = p.q_start;
+  const bool split = p.sparse && kb < p.s && p.nsplit > 1;
+  if (split) {  // sink tile: rows split by whole query blocks, walked in the local tiles' rotation
+    if (p1 > p0) {
+      const int ma = p0 / p.b, nb = (p1 - 1) / p.b - ma + 1, cb = (nb + p.nsplit - 1) / p.nsplit;
+      const int a = (ma + (int)blockIdx.y * cb) * p.b, e = a + cb * p.b;
+      if (a > p0) p0 = a;
+      if (e < p1) p1 = e;
+    }
+  } else if (blockIdx.y > 0) {
+    return;  // both CTAs of the pair
+  }
+  RowIter it;
+  it.L = p.sparse && (split || kb >= p.s) ? p.l : 1;
+  it.m0 = p0 / p.b;
+  it.m1 = (p1 - 1) / p.b;
+  it.p0 = p0;
+  it.p1 = p1;
+  it.R0 = p1 > p0 ? (p0 - p.q_start) * H : 0;
+  it.R1 = p1 > p0 ? (p1 - p.q_start) * H : 0;
+  it.qs = p.q_start;
+  it.H = H;
+  it.b = p.b;
+  it.step = kPRows;
+  it.start();
+  const bool any = it.valid();
+
+  auto bar = [&](int i) { return sbase + C::kOffBar + 8 * i; };
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::kOffTmemPtr);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(bar(C::kBarFull + i), 1);
+      mbar_init(bar(C::kBarEmpty + i), 1);
+    }
+    mbar_init(bar(C::kBarK), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(C::kBarSFull + i), 1);
+      mbar_init(bar(C::kBarSFree + i), 16);  // 8 warps of each CTA (leader's barrier)
+    }
+    mbar_init(bar(C::kBarPLocal), 4);
+    mbar_init(bar(C::kBarPStaged), 4);
+    mbar_init(bar(C::kBarPRecv), 1);
+    mbar_init(bar(C::kBarPFull), 2);  // the transfer warp of each CTA (leader's barrier)
+    mbar_init(bar(C::kBarPFree), 1);
+    mbar_init(bar(C::kBarAcc), 1);
+    fence_mbar_init();
+    if (any) mbar_arrive_expect_tx(bar(C::kBarPRecv), C::kStBytes);  // tile 0's rows from the partner
+  }
+  if (warp == kPProd && lane == 0) {
+    prefetch_tmap(&p.q_map);
+    prefetch_tmap(&p.o_map);
+    prefetch_tmap(&p.k_map);
+  }
+  if (warp == kPMma) tmem_alloc<2>(smem_u32(tmem_ptr), 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+
+  if (warp == kPProd) {
+    // ------------------------------------------------------------------ TMA producer (each CTA)
+    if (any) {
+      const uint64_t pol_k = policy_evict_last(), pol = policy_evict_normal();
+      const uint32_t full_l = mapa(bar(C::kBarFull), 0);
+      if (elect_one()) {
+        if (rank == 0) mbar_arrive_expect_tx(bar(C::kBarK), 2 * C::kKBytes);
+        tma_load_4d_pair(sbase + C::kOffK, &p.k_map, 0, j0 + 64 * (int)rank, 0, bi, mapa(bar(C::kBarK), 0), pol_k);
+      }
+      __syncwarp();
+      uint32_t slot = 0, ph = 0;
+      auto load_pair = [&](const CUtensorMap* m, int row, int pair) {
+        mbar_wait(bar(C::kBarEmpty + slot), ph ^ 1);
+        if (elect_one()) {
+          if (rank == 0) mbar_arrive_expect_tx(bar(C::kBarFull + slot), 2 * kPairBytes);
+          tma_load_4d_pair(sbase + C::kOffRing + slot * kPairBytes, m, 0, row, 2 * pair, bi, full_l + 8 * slot, pol);
+        }
+        __syncwarp();
+        if (++slot == C::kStages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      };
+      // first pass: this CTA's 128 rows (Q for S, or dO for dP); gradient pass: all 256 rows of this CTA's
+      // dims of each 256-dim group (dO for dV^T, Q for dK^T)
+      auto load_first = [&](int rb) {
+        for (int q = 0; q < C::kFirstItems; ++q) load_pair(kDvK ? &p.q_map : &p.o_map, rb + kRows * (int)rank, q);
+      };
+      auto load_grad = [&](int rb) {
+        for (int g = 0; g < C::kGroups; ++g)
+          for (int h = 0; h < 2; ++h) load_pair(kDvK ? &p.o_map : &p.q_map, rb + kRows * h, 2 * g + (int)rank);
+      };
+      RowIter ia = it;
+      load_first(ia.rb);
+      ia.advance();
+      for (RowIter ib = it; ib.valid(); ib.advance()) {
+        if (ia.valid()) {
+          load_first(ia.rb);
+          ia.advance();
+        }
+        load_grad(ib.rb);
+      }
+      // drain: the last commits to this CTA's Empty barriers land before it can exit
+      for (int i = 0; i < C::kStages; ++i) {
+        mbar_wait(bar(C::kBarEmpty + slot), ph ^ 1);
+        if (++slot == C::kStages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == kPMma) {
+    // ------------------------------------------------------------------ UMMA issuer (leader CTA)
+    if (any && rank == 0) {
+      constexpr uint32_t id_s = idesc_bf16_f32(256, kPKeys, false, false);
+      constexpr uint32_t id_t = idesc_bf16_f32(256, kPKeys, true, true);
+      mbar_wait(bar(C::kBarK), 0);
+      tc_fence_after();
+      uint32_t slot = 0, ph = 0;
+      auto take = [&]() {
+        mbar_wait(bar(C::kBarFull + slot), ph);
+        tc_fence_after();
+      };
+      auto release = [&]() {
+        if (elect_one()) umma_commit_pair_mc(bar(C::kBarEmpty + slot), 3);
+        __syncwarp();
+        if (++slot == C::kStages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      };
+      // S = Q K^T (dV kernel) or dP = dO V^T (dK kernel) of row tile tc into S buffer tc % kSBufs
+      auto issue_first = [&](int tc) {
+        const int buf = tc % C::kSBufs, use = tc / C::kSBufs;
+        BTRACE(0, tc);
+        mbar_wait(bar(C::kBarSFree + buf), (use & 1) ^ 1);
+        BTRACE(1, tc);
+        tc_fence_after();
+        const uint32_t d = tmem + C::kTmemS + 128 * buf;
+        for (int q = 0; q < C::kFirstItems; ++q) {
+          take();
+          if (elect_one()) {
+            const int nk = kDvK && q == kQPairs - 1 ? 4 : 8;  // Q chunk 9 is the zero-filled half of the last pair
+            for (int k = 0; k < nk; ++k) {
+              const uint32_t ch = 2 * q + (k >> 2), kk = k & 3;
+              umma_bf16_pair(d, sdesc_sw128(sbase + C::kOffRing + slot * kPairBytes + (k >> 2) * 16384 + 32 * kk, 16, 1024),
+                             sdesc_sw128(sbase + C::kOffK + ch * (64 * 128) + 32 * kk, 16, 1024), id_s, (q | k) != 0);
+            }
+          }
+          release();
+        }
+        if (elect_one()) umma_commit_pair_mc(bar(C::kBarSFull + buf), 3);
+        __syncwarp();
+        BTRACE(2, tc);
+      };
+      // dV^T += dO^T P or dK^T += Q^T dS over the tile's 256 rows (P / dS rows 128 h .. of both CTAs)
+      auto issue_grad = [&](int tc) {
+        BTRACE(3, tc);
+        mbar_wait_acquire_cluster(bar(C::kBarPFull), tc & 1);  // both CTAs' P halves are in place
+        BTRACE(4, tc);
+        tc_fence_after();
+        const uint32_t pb = sbase + C::kOffP;
+        for (int g = 0; g < C::kGroups; ++g)
+          for (int h = 0; h < 2; ++h) {
+            take();
+            if (elect_one()) {
+              for (int kr = 0; kr < 8; ++kr)
+                umma_bf16_pair(tmem + C::kTmemAcc + 128 * g,
+                               sdesc_sw128(sbase + C::kOffRing + slot * kPairBytes + 2048 * kr, 16384, 1024),
+                               sdesc_sw128(pb + 2048 * (8 * h + kr), 16, 1024), id_t, (tc | h | kr) != 0);
+            }
+            release();
+          }
+        if (elect_one()) umma_commit_pair_mc(bar(C::kBarPFree), 3);
+        __syncwarp();
+        BTRACE(5, tc);
+      };
+      RowIter ia = it;
+      issue_first(0);
+      ia.advance();
+      int ta = 1, tc = 0;
+      for (RowIter ib = it; ib.valid(); ib.advance(), ++tc) {
+        if (ia.valid()) {
+          issue_first(ta++);
+          ia.advance();
+        }
+        issue_grad(tc);
+      }
+      if (elect_one()) umma_commit_pair_mc(bar(C::kBarAcc), 3);
+      __syncwarp();
+      // the last S-buffer releases (remote arrivals from the partner) land before this CTA can exit
+      for (int u = ta - C::kSBufs; u < ta; ++u)
+        if (u >= 0) mbar_wait(bar(C::kBarSFree + u % C::kSBufs), (u / C::kSBufs) & 1);
+    }
+  } else if (warp == kPXfer) {
+    // ------------------------------------------------------------------ the staged half to the partner
+    if (any) {
+      const uint32_t pfull0 = mapa(bar(C::kBarPFull), 0);
+      const uint32_t dst = mapa(sbase + C::kOffP + (uint32_t)(kRows * rank) * 128, partner);
+      const uint32_t precv = mapa(bar(C::kBarPRecv), partner);
+      RowIter ix = it;
+      for (int tc = 0; ix.valid(); ix.advance(), ++tc) {
+        const uint32_t ph = (uint32_t)tc & 1;
+        mbar_wait(bar(C::kBarPStaged), ph);
+        if (lane == 0) bulk_copy_to_cluster(dst, sbase + C::kOffSt, C::kStBytes, precv);
+        mbar_wait_spin(bar(C::kBarPRecv), ph);  // the partner's rows of this CTA's half landed
+        mbar_wait(bar(C::kBarPLocal), ph);      // and this CTA's own rows are written
+        if (lane == 0) {
+          RowIter nx = ix;
+          nx.advance();
+          if (nx.valid()) mbar_arrive_expect_tx(bar(C::kBarPRecv), C::kStBytes);  // the next tile's, armed ahead
+          mbar_arrive_release_cluster(pfull0);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp < 8) {
+    // ------------------------------------------------------------------ P or dS (thread = row, 64 keys)
+    const int q = warp & 3, kh = warp >> 2, row = 32 * q + lane;
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+    const int rows = p.n_q * H;
+    const bool jsink = !p.sparse || kb < p.s;
+    const bool own = kh == (int)rank;  // keys 64 kh .. belong to CTA kh
+    const uint32_t sfree0 = mapa(bar(C::kBarSFree), 0);
+    const uint32_t pdst = own ? sbase + C::kOffP + (uint32_t)(kRows * rank + row) * 128 : sbase + C::kOffSt + row * 128;
+    const uint32_t sw = (uint32_t)(row & 7);
+    struct RowIn {
+      bool rv, win;
+      int pos;
+      float lse2, Dr;
+      uint4* ds;  // this row's 64 slots of block kb for key half kh in the dS row buffer
+    };
+    auto row_in = [&](const RowIter& ri) {
+      RowIn x;
+      const int r = ri.rb + kRows * (int)rank + row;
+      x.rv = ri.valid() && r < ri.re;
+      const int rr = x.rv ? r : 0, t = div_h(p, rr), h = rr - t * H;
+      x.pos = p.q_start + t;
+      x.lse2 = (kDvK && x.rv) ? p.lse[((int64_t)bi * H + h) * p.n_q + t] * kLog2e : 0.f;
+      x.Dr = (!kDvK && x.rv) ? p.D[(int64_t)bi * rows + rr] : 0.f;
+      x.win = jsink || kb >= x.pos / p.b - p.l + 1;
+      x.ds = nullptr;
+      if (p.ds && x.rv) {
+        int lbq = x.pos / p.b - p.l + 1;
+        if (lbq < p.s) lbq = p.s;
+        const int W = (p.s + p.l) * p.b;
+        const int slot = (kb < p.s ? j0 : p.s * p.b + (kb - lbq) * p.b) + 64 * kh;
+        x.ds = reinterpret_cast<uint4*>(p.ds + ((int64_t)bi * rows + rr) * W + slot);
+      }
+      return x;
+    };
+    uint32_t pn[32];  // dK kernel: the next tile's P (bf16 pairs), loaded one tile ahead
+    auto load_p = [&](const RowIn& x) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint4 v = x.ds ? x.ds[u] : make_uint4(0, 0, 0, 0);
+        pn[4 * u] = v.x;
+        pn[4 * u + 1] = v.y;
+        pn[4 * u + 2] = v.z;
+        pn[4 * u + 3] = v.w;
+      }
+    };
+    RowIn cur = row_in(it);
+    if (!kDvK) load_p(cur);
+    int tc = 0;
+    for (; it.valid(); ++tc) {
+      const int buf = tc % C::kSBufs, use = tc / C::kSBufs;
+      uint32_t pk[32];
+      if (!kDvK) {
+#pragma unroll
+        for (int u = 0; u < 32; ++u) pk[u] = pn[u];
+      }
+      mbar_wait(bar(C::kBarSFull + buf), use & 1);
+      if (warp == 0) BTRACE(6, tc);
+      tc_fence_after();
+      uint32_t sv[64];
+      {
+        uint32_t (&s0)[32] = *reinterpret_cast<uint32_t (*)[32]>(&sv[0]);
+        uint32_t (&s1)[32] = *reinterpret_cast<uint32_t (*)[32]>(&sv[32]);
+        tmem_ld32(tl + C::kTmemS + 128 * buf + 64 * kh, s0);
+        tmem_ld32(tl + C::kTmemS + 128 * buf + 64 * kh + 32, s1);
+      }
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(sfree0 + 8 * buf);
+      if (warp == 0) BTRACE(7, tc);
+      // the next tile's row inputs (and P) while this tile is processed
+      RowIter nx = it;
+      nx.advance();
+      const RowIn nxt = row_in(nx);
+      if (!kDvK) load_p(nxt);
+#pragma unroll
+      for (int c = 0; c < 64; c += 2) {
+        float v2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = j0 + 64 * kh + c + e;
+          const bool ok = cur.rv && cur.win && j < p.n_kv && (!p.causal || j <= cur.pos);
+          if (kDvK) {
+            v2[e] = ok ? ex2(fmaf(__uint_as_float(sv[c + e]), p.sl2, -cur.lse2)) : 0.f;
+          } else {
+            const uint32_t w2 = pk[c >> 1];
+            const float pv = e ? __uint_as_float(w2 & 0xFFFF0000u) : __uint_as_float(w2 << 16);
+            v2[e] = pv * (__uint_as_float(sv[c + e]) - cur.Dr);
+          }
+        }
+        pk[c >> 1] = pack_bf16x2(v2[0], v2[1]);
+      }
+      if (warp == 0) BTRACE(8, tc);
+      mbar_wait(bar(C::kBarPFree), (tc & 1) ^ 1);  // both CTAs' P buffers (and the staging) are free again
+      if (warp == 0) BTRACE(9, tc);
+      // row of 128 B = 8 x 16-B units, SWIZZLE_128B: unit u at (u ^ row & 7)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) st_shared_v4(pdst + ((u ^ sw) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(bar(own ? C::kBarPLocal : C::kBarPStaged));
+      if (warp == 0) BTRACE(10, tc);
+      if (cur.ds) {  // P (dV kernel) or dS (dK kernel) of the row's 64 keys into the dS row buffer
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cur.ds[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      }
+      it = nx;
+      cur = nxt;
+    }
+    // ------------------------------------------------------------------ epilogue: TMEM lane = dim, column = key
+    if (any) {
+      mbar_wait(bar(C::kBarPFree), (tc & 1) ^ 1);  // the last gradient commit (it precedes Acc) has landed
+      mbar_wait(bar(C::kBarAcc), 0);
+      tc_fence_after();
+    }
+    for (int g = 0; g < C::kGroups; ++g) {
+      const int d0 = 256 * g + 128 * (int)rank + 32 * q, dim = d0 + lane;
+      if (d0 >= (kDvK ? kDv : kDqk)) continue;  // warp-uniform: the zero-filled dims of dK^T's third group
+      const float sc = kDvK ? 1.f : p.scale;
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t v[32];
+        if (any) {
+          tmem_ld32(tl + C::kTmemAcc + 128 * g + 64 * kh + 32 * hf, v);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) v[c] = 0u;
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int j = j0 + 64 * kh + 32 * hf + c;
+          if (j >= p.n_kv) continue;
+          const float x = __uint_as_float(v[c]) * sc;
+          if (split) {  // partials in the 32-key tile layout of the sink reduce: [B][n_sink][nsplit][32][1088]
+            const int t32 = j >> 5, kl = j & 31;
+            p.part[((((int64_t)bi * p.n_sink + t32) * p.nsplit + blockIdx.y) * kKeys + kl) * kDkv + (kDvK ? kDqk : 0) + dim] = x;
+          } else if (kDvK) {
+            p.dv[((int64_t)bi * p.n_kv + j) * kDv + dim] = x;
+          } else {
+            p.dk[((int64_t)bi * p.n_kv + j) * kDqk + dim] = x;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == kPMma) {
+    tc_fence_after();
+    tmem_dealloc<2>(tmem, 512);
+  }
+}
+
 // ---------------------------------------------------------------------------------------------- dQ = dS K
 // SSA only: dQ[128 rows, 192-dim slice] = scale * DS[rows, slots] K[slots -> keys, slice] as a tcgen05 GEMM
 // (M128 N192 K16, A = DS K-major, B = K MN-major over 3 64-dim atoms) from the dS rows the key kernel wrote:
@@ -1039,9 +1521,76 @@ cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk
 // 64-key tiles (two kernels, dV then dK): the tile must lie in one block (b % 64 == 0) when sparse
 bool backward_key64_eligible(const AttnProblem& a) { return !a.sparse || a.b % k64Keys == 0; }
 
+unsigned long long* g_bwd_trace = nullptr;  // loza_debug_set_bwd_trace
+int g_bwd_trace_cluster = 0, g_bwd_trace_mode = 0;
+
+// 128-key CTA-pair kernels (dV, then dK reading P back from the dS row buffer): SSA with b == 128
+static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
+                                      float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st,
+                                      cudaEvent_t d_ready) {
+  TcBwdParams p;
+  const auto& kv = a.kv.seg[0];
+  const uint64_t rows = (uint64_t)a.n_q * a.heads;
+  TcBwdParams pk;  // the dK kernel's: its K tile is V's 8 chunks
+  if (!encode_4d_chunks(&p.q_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 2) ||
+      !encode_4d_chunks(&p.o_map, dout, kDv, rows, a.batch, a.o_sh, a.o_sb, kRows, 2) ||
+      !encode_4d_chunks(&p.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, 64, 9) ||
+      !encode_4d_chunks(&pk.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, 64, 8))
+    return cudaErrorInvalidValue;
+  p.lse = a.lse;
+  p.D = D;
+  p.dk = dk;
+  p.dv = dv;
+  p.part = part;
+  p.ds = ds;
+  p.batch = a.batch;
+  p.n_q = a.n_q;
+  p.heads = a.heads;
+  p.n_kv = (int32_t)a.n_kv;
+  p.q_start = (int32_t)a.q_start;
+  p.scale = a.scale;
+  p.sl2 = a.scale * kLog2e;
+  p.sparse = a.sparse;
+  p.causal = a.causal;
+  p.s = a.s;
+  p.l = a.l;
+  p.b = a.b;
+  p.nsplit = nsplit;
+  p.n_sink = n_sink;
+  {
+    uint32_t l = 0;
+    while ((1ull << l) < (uint64_t)a.heads) ++l;
+    p.h_p = 31 + l;
+    p.h_m = (uint32_t)(((1ull << p.h_p) + a.heads - 1) / a.heads);
+  }
+  p.trace = g_bwd_trace_mode == kPairDv ? g_bwd_trace : nullptr;
+  p.trace_cluster = g_bwd_trace_cluster;
+  const CUtensorMap k8 = pk.k_map;
+  pk = p;
+  pk.k_map = k8;
+  pk.trace = g_bwd_trace_mode == kPairDk ? g_bwd_trace : nullptr;
+  const int64_t kt = (a.n_kv + kPKeys - 1) / kPKeys;
+  const bool use_part = a.sparse && nsplit > 1;
+  const dim3 grid((unsigned)(2 * a.batch * kt), use_part ? nsplit : 1);
+  cudaError_t e = cudaFuncSetAttribute(bwd_pair_tc_kernel<kPairDv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       PairCfg<kPairDv>::kSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(bwd_pair_tc_kernel<kPairDk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PairCfg<kPairDk>::kSmem);
+  if (e != cudaSuccess) return e;
+  bwd_pair_tc_kernel<kPairDv><<<grid, kPThreads, PairCfg<kPairDv>::kSmem, st>>>(p);
+  count_launch();
+  if (d_ready && (e = cudaStreamWaitEvent(st, d_ready, 0)) != cudaSuccess) return e;  // D (side stream) for dS
+  bwd_pair_tc_kernel<kPairDk><<<grid, kPThreads, PairCfg<kPairDk>::kSmem, st>>>(pk);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
                                 float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st,
-                                cudaEvent_t d_ready) {
+                                cudaEvent_t d_ready, bool allow_pair) {
+  if (allow_pair && ds && a.sparse && a.b == kPKeys)
+    return launch_bwd_pair_tc(a, dout, dk, dv, D, part, ds, nsplit, n_sink, st, d_ready);
   TcBwdParams p;
   const auto& kv = a.kv.seg[0];
   const uint64_t rows = (uint64_t)a.n_q * a.heads;
@@ -1158,3 +1707,11 @@ cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq
 }
 
 }  // namespace loza
+
+// debug hook (not part of include/loza.h): clock64 timeline of pair cluster `cluster` of the backward pair
+// kernel `mode` (1 dV, 2 dK) into dev_ptr (tools/trace_bwd.py)
+extern "C" void loza_debug_set_bwd_trace(void* dev_ptr, int32_t cluster, int32_t mode) {
+  loza::g_bwd_trace = (unsigned long long*)dev_ptr;
+  loza::g_bwd_trace_cluster = cluster;
+  loza::g_bwd_trace_mode = mode;
+}

@@ -96,10 +96,11 @@ cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk
 // SSA dS-row buffer [B][n_q*H][(s+l)*b] bf16 (written by the tcgen05 key kernel) and dQ = dS K on tcgen05
 bool backward_ds_eligible(const AttnProblem& a);
 bool backward_key64_eligible(const AttnProblem& a);
-// d_ready (nullable): an event the dK kernel waits for (D computed on another stream, beside the dV kernel)
+// d_ready (nullable): an event the dK kernel waits for (D computed on another stream, beside the dV kernel).
+// With the dS row buffer and b == 128 the 128-key CTA-pair kernels run instead unless allow_pair is false.
 cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
                                 float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st,
-                                cudaEvent_t d_ready = nullptr);
+                                cudaEvent_t d_ready = nullptr, bool allow_pair = true);
 size_t backward_ds_bytes(const AttnProblem& a);
 cudaError_t launch_bwd_D(const AttnProblem& a, const void* dout, float* D, cudaStream_t st);
 cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq, cudaStream_t st);

@@ -145,7 +145,8 @@ def test_backward_tiled_fp32_h8(sparse, causal, q0):
     (True, True, 0, 16, 1280, (1, 2, 256), 1, False),   # b = 256: 8 key tiles per block, 2 splits
 ])
 def test_backward_mla_mma(sparse, causal, q0, H, n, pat, B, ofwd):
-    """The tensor-core backward (SSA: D, tcgen05 key kernel writing dS rows, tcgen05 dQ = dS K; full attention:
+    """The tensor-core backward (SSA: D, tcgen05 key kernels writing dS rows -- the 128-key CTA-pair kernels when
+    b = 128, 64-key kernels otherwise -- and tcgen05 dQ = dS K; full attention:
     the attn_bwd_mma.cu row kernel + tcgen05 key kernel; bf16, 576/512, V = KV[:, :512]) against the fp64 oracle
     backward, every row and key, bf16 tolerance (2e-2 normwise); deterministic across calls. ofwd: O and LSE
     from the oracle forward (rounded to bf16 / fp32), for row counts the bf16 forward does not take."""
@@ -201,12 +202,13 @@ def test_backward_mla_simt_forced():
 
 
 @pytest.mark.parametrize("env", [{"LOZA_TEST_BACKWARD_KERNEL": "2"}, {"LOZA_TEST_BACKWARD_KERNEL": "3"},
-                                 {"LOZA_TEST_BACKWARD_KERNEL": "4"}])
+                                 {"LOZA_TEST_BACKWARD_KERNEL": "4"}, {"LOZA_TEST_BACKWARD_KERNEL": "5"}])
 def test_backward_mma_paths_forced(env):
     """The other key / dQ kernels kept reachable through the MLA parity cases (test knob backward,
     loza_debug_force_kernel): 2 = the warp-MMA key kernel and row kernel of attn_bwd_mma.cu instead of the
     tcgen05 key kernels and dS GEMM; 3 = tcgen05 key kernels, dQ by the row kernel instead of the tcgen05 dS
-    GEMM; 4 = the 32-key tcgen05 key kernel (dK and dV in one pass) instead of the 64-key dV / dK pair."""
+    GEMM; 4 = the 32-key tcgen05 key kernel (dK and dV in one pass) instead of the 64-key dV / dK pair; 5 = the
+    64-key dV / dK kernels where the 128-key CTA-pair kernels are the default (SSA, b = 128)."""
     import os
     import subprocess
     import sys
