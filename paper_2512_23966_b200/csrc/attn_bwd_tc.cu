@@ -49,6 +49,7 @@ struct TcBwdParams {
   CUtensorMap q_map;  // {64, n_q*H rows, 9 chunks, B}, box {64, 128, 2, 1}
   CUtensorMap o_map;  // dO: {64, n_q*H, 8, B}, box {64, 128, 2, 1}
   CUtensorMap k_map;  // {64, n_kv, 9, B}, box {64, 32, 9, 1}
+  CUtensorMap q4_map, q1_map, o4_map;  // pair kernels: q / dO boxes {64, 64, 4 (q1: 1), 1}
   const float* lse;
   const float* D;
   float* dk;
@@ -805,31 +806,33 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
 // ------------------------------------------------------------------------ key side, 128-key pair tiles
 // The 64-key kernels above move every 128-row tile of Q and dO through one SM per 64 keys (288 KB per tile
 // for the dV kernel) and run M128 N64 UMMAs (48 cycles, smem-operand bound). Here a CTA pair (cta_group::2)
-// owns the 128 keys of one b-block (b = 128) and streams 256-row tiles, CTA r staging 64 keys (the N half of
-// every B operand) and half of each tile's operands:
+// owns the 128 keys of one b-block (b = 128): CTA r stages 64 of them (the N half of every B operand) and
+// half of each 128-row tile's operands:
 //   dV pair kernel (MODE kPairDv):
-//     S   [256 rows x 128 keys] = Q K^T    M256 N128 (A = CTA r's 128 rows of Q, B = its 64 keys): CTA r's TMEM
-//                                           holds S of its rows for all 128 keys
-//     P   = exp2(S scale log2e - LSE log2e) by 8 warps per CTA (thread = row, 64 keys); the P of CTA c's keys
+//     S   [128 rows x 128 keys] = Q K^T    M128 N128 (A = CTA r's 64 rows of Q, B = its 64 keys); CTA r's TMEM
+//                                           holds S of its rows folded: lanes 0-63 keys 0-63, lanes 64-127 keys
+//                                           64-127 (64 columns per S buffer, four buffers: S runs three row
+//                                           tiles ahead of the gradient UMMAs)
+//     P   = exp2(S scale log2e - LSE log2e) by 8 warps per CTA (thread = row x 32 keys); the P of CTA c's keys
 //           must end up in CTA c (the N half of the next B operand): the own half is written in place, the
-//           other half staged and moved by one 16 KB bulk DSMEM copy. The row's values also go to the dS row
+//           other half staged and moved by one 8 KB bulk DSMEM copy. The row's values also go to the dS row
 //           buffer (the dK kernel reads P there).
 //     dV^T [512 x 128] += dO^T P           M256 N128 per 256-dim group (A = dO^T MN-major: CTA r stages dims
-//                                           256 g + 128 r .. + 127 of all 256 rows)
+//                                           256 g + 128 r .. + 127 of all 128 rows)
 //   dK pair kernel (MODE kPairDk, SSA):
-//     dP  = dO V^T                          M256 N128 (A = CTA r's 128 rows of dO, B = V of its 64 keys)
+//     dP  = dO V^T                          M128 N128 (A = CTA r's 64 rows of dO, B = V of its 64 keys), two
+//                                           buffers
 //     dS  = P (dP - D) (P read back from the dS row buffer), into the dS row buffer and, split by keys as above,
 //           into the two CTAs' dS buffers
 //     dK^T [576 x 128] += Q^T dS            three M256 N128 groups (dims 512.. of the third: CTA 0 stages
 //                                           chunk 8 and a zero-filled chunk 9, CTA 1 two zero-filled chunks)
-// Per SM and 128 x 128 (row, key) pairs the dV kernel moves 288 KB (the 64-key kernel: 576 KB) and the dK kernel
-// 320 KB (64-key: 588 KB), and every UMMA is M256 N128 (64 cycles for 2 x 128 x 128 x 16 MACs).
-// TMEM per CTA: dV kernel S 2 x 128 + dV^T 2 x 128 columns; dK kernel dK^T 3 x 128 + dP 128 (single-buffered:
-// the dS warps release it right after their TMEM loads). SMEM: ring 3 x 32 KB, K tile 72 KB (dV: 9 chunks) or
-// 64 KB (dK: V's 8), P / dS 32 KB, staging 16 KB. Warps 0-7 P / dS and the epilogue (warp w: TMEM lane quarter
-// w % 4, key half w / 4), warp 8 TMA, warp 9 UMMA issue (leader) and TMEM allocation, warp 10 the DSMEM copy.
+// Per SM and 128 x 128 (row, key) pairs the dV kernel moves 136 KB of Q / dO (the 64-key kernel: 576 KB) and
+// the dK kernel 160 KB (64-key: 588 KB). TMEM per CTA: dV kernel S 4 x 64 + dV^T 2 x 128 columns; dK kernel
+// dK^T 3 x 128 + dP 2 x 64. SMEM: ring 3 x 32 KB, K tile 72 KB (dV: 9 chunks) or 64 KB (dK: V's 8), P / dS
+// 2 x 16 KB, staging 2 x 8 KB. Warps 0-7 P / dS and the epilogue (warp w: TMEM lane quarter w % 4, column half w / 4),
+// warp 8 TMA, warp 9 UMMA issue (leader) and TMEM allocation, warp 10 the DSMEM copy.
 constexpr int kPairDv = 1, kPairDk = 2;
-constexpr int kPKeys = 128, kPRows = 2 * kRows;  // keys per pair tile, rows per pair row tile
+constexpr int kPKeys = 128, kPHalf = 64;  // keys per pair tile; rows of a 128-row tile per CTA
 constexpr int kPThreads = 352, kPProd = 8, kPMma = 9, kPXfer = 10;
 template <int MODE>
 struct PairCfg {
@@ -837,20 +840,22 @@ struct PairCfg {
   static constexpr int kStages = 3;
   static constexpr int kKChunks = kDv ? 9 : 8;             // the K tile (S needs 576 dims, dP only V's 512)
   static constexpr int kKBytes = kKChunks * 64 * 128;      // [chunks][64 keys][64 dims]
-  static constexpr int kPBytes = kPRows * 128;             // P / dS: [256 rows][64 keys] bf16, SW128
-  static constexpr int kStBytes = kRows * 128;             // staging: [128 rows][the partner's 64 keys]
-  static constexpr int kOffRing = 0, kOffK = kStages * kPairBytes, kOffP = kOffK + kKBytes, kOffSt = kOffP + kPBytes,
-                       kOffBar = kOffSt + kStBytes;
+  static constexpr int kPBytes = kRows * 128;              // P / dS: [128 rows][64 keys] bf16, SW128
+  static constexpr int kStBytes = kPHalf * 128;            // staging: [64 rows][the partner's 64 keys]
+  // P / dS and staging double-buffered (row tile tc uses buffer tc & 1): the gradient UMMAs of tile tc - 1
+  // and the DSMEM copy of tile tc overlap the P of tile tc + 1
+  static constexpr int kOffRing = 0, kOffK = kStages * kPairBytes, kOffP = kOffK + kKBytes,
+                       kOffSt = kOffP + 2 * kPBytes, kOffBar = kOffSt + 2 * kStBytes;
+  static constexpr int kSBufs = kDv ? 4 : 2, kAhead = kSBufs - 1;  // S / dP buffers, first-pass lookahead
   static constexpr int kBarFull = 0, kBarEmpty = kStages, kBarK = 2 * kStages, kBarSFull = kBarK + 1,
-                       kBarSFree = kBarSFull + 2, kBarPLocal = kBarSFree + 2, kBarPStaged = kBarPLocal + 1,
-                       kBarPRecv = kBarPStaged + 1, kBarPFull = kBarPRecv + 1, kBarPFree = kBarPFull + 1,
-                       kBarAcc = kBarPFree + 1, kNumBars = kBarAcc + 1;
+                       kBarSFree = kBarSFull + kSBufs, kBarPLocal = kBarSFree + kSBufs, kBarPStaged = kBarPLocal + 2,
+                       kBarPRecv = kBarPStaged + 2, kBarPFull = kBarPRecv + 2, kBarPFree = kBarPFull + 2,
+                       kBarAcc = kBarPFree + 2, kNumBars = kBarAcc + 1;
   static constexpr int kOffTmemPtr = kOffBar + 8 * kNumBars;
   static constexpr int kSmem = kOffTmemPtr + 16 + 1024;
-  static constexpr int kFirstItems = kDv ? kQPairs : kOPairs;  // Q (S) or dO (dP) of this CTA's 128 rows
-  static constexpr int kGroups = kDv ? 2 : 3;                  // 256-dim M groups of dV^T / dK^T
+  static constexpr int kFirstItems = kDv ? 3 : 2;  // Q (chunks 0-3, 4-7, 8) or dO (0-3, 4-7) of this CTA's 64 rows
+  static constexpr int kGroups = kDv ? 2 : 3;      // 256-dim M groups of dV^T / dK^T
   static constexpr uint32_t kTmemS = kDv ? 0 : 384, kTmemAcc = kDv ? 256 : 0;
-  static constexpr int kSBufs = kDv ? 2 : 1;
 };
 static_assert(PairCfg<kPairDv>::kSmem <= 232448 && PairCfg<kPairDk>::kSmem <= 232448, "smem");
 
@@ -906,7 +911,6 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
   it.qs = p.q_start;
   it.H = H;
   it.b = p.b;
-  it.step = kPRows;
   it.start();
   const bool any = it.valid();
 
@@ -918,23 +922,28 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       mbar_init(bar(C::kBarEmpty + i), 1);
     }
     mbar_init(bar(C::kBarK), 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::kSBufs; ++i) {
       mbar_init(bar(C::kBarSFull + i), 1);
       mbar_init(bar(C::kBarSFree + i), 16);  // 8 warps of each CTA (leader's barrier)
     }
-    mbar_init(bar(C::kBarPLocal), 4);
-    mbar_init(bar(C::kBarPStaged), 4);
-    mbar_init(bar(C::kBarPRecv), 1);
-    mbar_init(bar(C::kBarPFull), 2);  // the transfer warp of each CTA (leader's barrier)
-    mbar_init(bar(C::kBarPFree), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(C::kBarPLocal + i), 4);
+      mbar_init(bar(C::kBarPStaged + i), 4);
+      mbar_init(bar(C::kBarPRecv + i), 1);
+      mbar_init(bar(C::kBarPFull + i), 2);  // the transfer warp of each CTA (leader's barrier)
+      mbar_init(bar(C::kBarPFree + i), 1);
+    }
     mbar_init(bar(C::kBarAcc), 1);
     fence_mbar_init();
-    if (any) mbar_arrive_expect_tx(bar(C::kBarPRecv), C::kStBytes);  // tile 0's rows from the partner
+    RowIter i1 = it;  // tiles 0 and 1: the partner's rows, armed ahead
+    for (int i = 0; i < 2 && i1.valid(); ++i, i1.advance()) mbar_arrive_expect_tx(bar(C::kBarPRecv + i), C::kStBytes);
   }
   if (warp == kPProd && lane == 0) {
     prefetch_tmap(&p.q_map);
     prefetch_tmap(&p.o_map);
     prefetch_tmap(&p.k_map);
+    prefetch_tmap(kDvK ? &p.q4_map : &p.o4_map);
+    if (kDvK) prefetch_tmap(&p.q1_map);
   }
   if (warp == kPMma) tmem_alloc<2>(smem_u32(tmem_ptr), 512);
   tc_fence_before();
@@ -954,11 +963,11 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       }
       __syncwarp();
       uint32_t slot = 0, ph = 0;
-      auto load_pair = [&](const CUtensorMap* m, int row, int pair) {
+      auto load = [&](const CUtensorMap* m, int row, int chunk, uint32_t bytes) {
         mbar_wait(bar(C::kBarEmpty + slot), ph ^ 1);
         if (elect_one()) {
-          if (rank == 0) mbar_arrive_expect_tx(bar(C::kBarFull + slot), 2 * kPairBytes);
-          tma_load_4d_pair(sbase + C::kOffRing + slot * kPairBytes, m, 0, row, 2 * pair, bi, full_l + 8 * slot, pol);
+          if (rank == 0) mbar_arrive_expect_tx(bar(C::kBarFull + slot), 2 * bytes);
+          tma_load_4d_pair(sbase + C::kOffRing + slot * kPairBytes, m, 0, row, chunk, bi, full_l + 8 * slot, pol);
         }
         __syncwarp();
         if (++slot == C::kStages) {
@@ -966,18 +975,27 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
           ph ^= 1;
         }
       };
-      // first pass: this CTA's 128 rows (Q for S, or dO for dP); gradient pass: all 256 rows of this CTA's
-      // dims of each 256-dim group (dO for dV^T, Q for dK^T)
+      // first pass: this CTA's 64 rows ([4 chunks][64 rows] boxes: Q for S, or dO for dP); gradient pass: the
+      // tile's 128 rows of this CTA's dims of each 256-dim group ([2 chunks][128 rows]: dO for dV^T, Q for dK^T)
       auto load_first = [&](int rb) {
-        for (int q = 0; q < C::kFirstItems; ++q) load_pair(kDvK ? &p.q_map : &p.o_map, rb + kRows * (int)rank, q);
+        const int r = rb + kPHalf * (int)rank;
+        if (kDvK) {
+          load(&p.q4_map, r, 0, kPairBytes);
+          load(&p.q4_map, r, 4, kPairBytes);
+          load(&p.q1_map, r, 8, kPairBytes / 4);
+        } else {
+          load(&p.o4_map, r, 0, kPairBytes);
+          load(&p.o4_map, r, 4, kPairBytes);
+        }
       };
       auto load_grad = [&](int rb) {
-        for (int g = 0; g < C::kGroups; ++g)
-          for (int h = 0; h < 2; ++h) load_pair(kDvK ? &p.o_map : &p.q_map, rb + kRows * h, 2 * g + (int)rank);
+        for (int g = 0; g < C::kGroups; ++g) load(kDvK ? &p.o_map : &p.q_map, rb, 2 * (2 * g + (int)rank), kPairBytes);
       };
       RowIter ia = it;
-      load_first(ia.rb);
-      ia.advance();
+      for (int i = 0; i < C::kAhead && ia.valid(); ++i) {
+        load_first(ia.rb);
+        ia.advance();
+      }
       for (RowIter ib = it; ib.valid(); ib.advance()) {
         if (ia.valid()) {
           load_first(ia.rb);
@@ -997,7 +1015,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
   } else if (warp == kPMma) {
     // ------------------------------------------------------------------ UMMA issuer (leader CTA)
     if (any && rank == 0) {
-      constexpr uint32_t id_s = idesc_bf16_f32(256, kPKeys, false, false);
+      constexpr uint32_t id_s = idesc_bf16_f32(128, kPKeys, false, false);
       constexpr uint32_t id_t = idesc_bf16_f32(256, kPKeys, true, true);
       mbar_wait(bar(C::kBarK), 0);
       tc_fence_after();
@@ -1014,21 +1032,21 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
           ph ^= 1;
         }
       };
-      // S = Q K^T (dV kernel) or dP = dO V^T (dK kernel) of row tile tc into S buffer tc % kSBufs
+      // S = Q K^T (dV kernel) or dP = dO V^T (dK kernel) of row tile tc into buffer tc % kSBufs
       auto issue_first = [&](int tc) {
         const int buf = tc % C::kSBufs, use = tc / C::kSBufs;
         BTRACE(0, tc);
         mbar_wait(bar(C::kBarSFree + buf), (use & 1) ^ 1);
         BTRACE(1, tc);
         tc_fence_after();
-        const uint32_t d = tmem + C::kTmemS + 128 * buf;
+        const uint32_t d = tmem + C::kTmemS + 64 * buf;
         for (int q = 0; q < C::kFirstItems; ++q) {
           take();
           if (elect_one()) {
-            const int nk = kDvK && q == kQPairs - 1 ? 4 : 8;  // Q chunk 9 is the zero-filled half of the last pair
+            const int nk = q < 2 ? 16 : 4;  // 4 chunks x 4 k steps (the dV kernel's third item: chunk 8 alone)
             for (int k = 0; k < nk; ++k) {
-              const uint32_t ch = 2 * q + (k >> 2), kk = k & 3;
-              umma_bf16_pair(d, sdesc_sw128(sbase + C::kOffRing + slot * kPairBytes + (k >> 2) * 16384 + 32 * kk, 16, 1024),
+              const uint32_t ch = 4 * q + (k >> 2), kk = k & 3;
+              umma_bf16_pair(d, sdesc_sw128(sbase + C::kOffRing + slot * kPairBytes + (k >> 2) * (kPHalf * 128) + 32 * kk, 16, 1024),
                              sdesc_sw128(sbase + C::kOffK + ch * (64 * 128) + 32 * kk, 16, 1024), id_s, (q | k) != 0);
             }
           }
@@ -1038,32 +1056,30 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
         __syncwarp();
         BTRACE(2, tc);
       };
-      // dV^T += dO^T P or dK^T += Q^T dS over the tile's 256 rows (P / dS rows 128 h .. of both CTAs)
+      // dV^T += dO^T P or dK^T += Q^T dS over the tile's 128 rows (P / dS rows 64 c .. from CTA c)
       auto issue_grad = [&](int tc) {
         BTRACE(3, tc);
-        mbar_wait_acquire_cluster(bar(C::kBarPFull), tc & 1);  // both CTAs' P halves are in place
+        mbar_wait_acquire_cluster(bar(C::kBarPFull + (tc & 1)), (tc >> 1) & 1);  // both CTAs' P halves are in place
         BTRACE(4, tc);
         tc_fence_after();
-        const uint32_t pb = sbase + C::kOffP;
-        for (int g = 0; g < C::kGroups; ++g)
-          for (int h = 0; h < 2; ++h) {
-            take();
-            if (elect_one()) {
-              for (int kr = 0; kr < 8; ++kr)
-                umma_bf16_pair(tmem + C::kTmemAcc + 128 * g,
-                               sdesc_sw128(sbase + C::kOffRing + slot * kPairBytes + 2048 * kr, 16384, 1024),
-                               sdesc_sw128(pb + 2048 * (8 * h + kr), 16, 1024), id_t, (tc | h | kr) != 0);
-            }
-            release();
+        const uint32_t pb = sbase + C::kOffP + (tc & 1) * C::kPBytes;
+        for (int g = 0; g < C::kGroups; ++g) {
+          take();
+          if (elect_one()) {
+            for (int kr = 0; kr < 8; ++kr)
+              umma_bf16_pair(tmem + C::kTmemAcc + 128 * g,
+                             sdesc_sw128(sbase + C::kOffRing + slot * kPairBytes + 2048 * kr, 16384, 1024),
+                             sdesc_sw128(pb + 2048 * kr, 16, 1024), id_t, (tc | kr) != 0);
           }
-        if (elect_one()) umma_commit_pair_mc(bar(C::kBarPFree), 3);
+          release();
+        }
+        if (elect_one()) umma_commit_pair_mc(bar(C::kBarPFree + (tc & 1)), 3);
         __syncwarp();
         BTRACE(5, tc);
       };
       RowIter ia = it;
-      issue_first(0);
-      ia.advance();
-      int ta = 1, tc = 0;
+      int ta = 0, tc = 0;
+      for (; ta < C::kAhead && ia.valid(); ++ta, ia.advance()) issue_first(ta);
       for (RowIter ib = it; ib.valid(); ib.advance(), ++tc) {
         if (ia.valid()) {
           issue_first(ta++);
@@ -1073,7 +1089,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       }
       if (elect_one()) umma_commit_pair_mc(bar(C::kBarAcc), 3);
       __syncwarp();
-      // the last S-buffer releases (remote arrivals from the partner) land before this CTA can exit
+      // the last buffer releases (remote arrivals from the partner) land before this CTA can exit
       for (int u = ta - C::kSBufs; u < ta; ++u)
         if (u >= 0) mbar_wait(bar(C::kBarSFree + u % C::kSBufs), (u / C::kSBufs) & 1);
     }
@@ -1081,43 +1097,49 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
     // ------------------------------------------------------------------ the staged half to the partner
     if (any) {
       const uint32_t pfull0 = mapa(bar(C::kBarPFull), 0);
-      const uint32_t dst = mapa(sbase + C::kOffP + (uint32_t)(kRows * rank) * 128, partner);
+      const uint32_t dst = mapa(sbase + C::kOffP + (uint32_t)(kPHalf * rank) * 128, partner);
       const uint32_t precv = mapa(bar(C::kBarPRecv), partner);
       RowIter ix = it;
       for (int tc = 0; ix.valid(); ix.advance(), ++tc) {
-        const uint32_t ph = (uint32_t)tc & 1;
-        mbar_wait(bar(C::kBarPStaged), ph);
-        if (lane == 0) bulk_copy_to_cluster(dst, sbase + C::kOffSt, C::kStBytes, precv);
-        mbar_wait_spin(bar(C::kBarPRecv), ph);  // the partner's rows of this CTA's half landed
-        mbar_wait(bar(C::kBarPLocal), ph);      // and this CTA's own rows are written
+        const uint32_t pb = (uint32_t)tc & 1, ph = ((uint32_t)tc >> 1) & 1;
+        mbar_wait(bar(C::kBarPStaged + pb), ph);
+        if (lane == 0)
+          bulk_copy_to_cluster(dst + pb * C::kPBytes, sbase + C::kOffSt + pb * C::kStBytes, C::kStBytes, precv + 8 * pb);
+        mbar_wait_spin(bar(C::kBarPRecv + pb), ph);  // the partner's rows of this CTA's half landed
+        mbar_wait(bar(C::kBarPLocal + pb), ph);      // and this CTA's own rows are written
         if (lane == 0) {
-          RowIter nx = ix;
-          nx.advance();
-          if (nx.valid()) mbar_arrive_expect_tx(bar(C::kBarPRecv), C::kStBytes);  // the next tile's, armed ahead
-          mbar_arrive_release_cluster(pfull0);
+          RowIter n2 = ix;
+          n2.advance();
+          n2.advance();
+          if (n2.valid()) mbar_arrive_expect_tx(bar(C::kBarPRecv + pb), C::kStBytes);  // tile tc + 2's, armed ahead
+          mbar_arrive_release_cluster(pfull0 + 8 * pb);
         }
         __syncwarp();
       }
     }
   } else if (warp < 8) {
-    // ------------------------------------------------------------------ P or dS (thread = row, 64 keys)
-    const int q = warp & 3, kh = warp >> 2, row = 32 * q + lane;
+    // ------------------------------------------------------------------ P or dS (thread = row x 32 keys)
+    // TMEM lane quarter q: rows 32 (q & 1) .., key half kh = q >> 1 (the fold of the M128 D); column half c
+    const int q = warp & 3, c = warp >> 2, kh = q >> 1, row = 32 * (q & 1) + lane;
     const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
     const int rows = p.n_q * H;
     const bool jsink = !p.sparse || kb < p.s;
     const bool own = kh == (int)rank;  // keys 64 kh .. belong to CTA kh
+    const int jk = j0 + 64 * kh + 32 * c;  // this thread's first key
     const uint32_t sfree0 = mapa(bar(C::kBarSFree), 0);
-    const uint32_t pdst = own ? sbase + C::kOffP + (uint32_t)(kRows * rank + row) * 128 : sbase + C::kOffSt + row * 128;
+    // this row's P in buffer 0 (buffer 1: + kPBytes / kStBytes)
+    const uint32_t pdst = own ? sbase + C::kOffP + (uint32_t)(kPHalf * rank + row) * 128 : sbase + C::kOffSt + row * 128;
+    const uint32_t pstride = own ? C::kPBytes : C::kStBytes;
     const uint32_t sw = (uint32_t)(row & 7);
     struct RowIn {
       bool rv, win;
       int pos;
       float lse2, Dr;
-      uint4* ds;  // this row's 64 slots of block kb for key half kh in the dS row buffer
+      uint4* ds;  // this row's 32 slots (keys jk ..) of block kb in the dS row buffer
     };
     auto row_in = [&](const RowIter& ri) {
       RowIn x;
-      const int r = ri.rb + kRows * (int)rank + row;
+      const int r = ri.rb + kPHalf * (int)rank + row;
       x.rv = ri.valid() && r < ri.re;
       const int rr = x.rv ? r : 0, t = div_h(p, rr), h = rr - t * H;
       x.pos = p.q_start + t;
@@ -1129,15 +1151,15 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
         int lbq = x.pos / p.b - p.l + 1;
         if (lbq < p.s) lbq = p.s;
         const int W = (p.s + p.l) * p.b;
-        const int slot = (kb < p.s ? j0 : p.s * p.b + (kb - lbq) * p.b) + 64 * kh;
+        const int slot = (kb < p.s ? j0 : p.s * p.b + (kb - lbq) * p.b) + (jk - j0);
         x.ds = reinterpret_cast<uint4*>(p.ds + ((int64_t)bi * rows + rr) * W + slot);
       }
       return x;
     };
-    uint32_t pn[32];  // dK kernel: the next tile's P (bf16 pairs), loaded one tile ahead
+    uint32_t pn[16];  // dK kernel: the next tile's P (bf16 pairs), loaded one tile ahead
     auto load_p = [&](const RowIn& x) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const uint4 v = x.ds ? x.ds[u] : make_uint4(0, 0, 0, 0);
         pn[4 * u] = v.x;
         pn[4 * u + 1] = v.y;
@@ -1147,71 +1169,78 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
     };
     RowIn cur = row_in(it);
     if (!kDvK) load_p(cur);
+    uint4* prev_ds = nullptr;  // the previous tile's dS row slots, stored one tile late: a proxy fence waits
+    uint32_t prev[16];         // for this thread's outstanding global stores
     int tc = 0;
     for (; it.valid(); ++tc) {
       const int buf = tc % C::kSBufs, use = tc / C::kSBufs;
-      uint32_t pk[32];
+      uint32_t pk[16];
       if (!kDvK) {
 #pragma unroll
-        for (int u = 0; u < 32; ++u) pk[u] = pn[u];
+        for (int u = 0; u < 16; ++u) pk[u] = pn[u];
       }
+      RowIter nx = it;
+      nx.advance();
+      const RowIn nxt = row_in(nx);  // the next tile's row inputs (and P) while this tile is processed
+      if (!kDvK) load_p(nxt);
       mbar_wait(bar(C::kBarSFull + buf), use & 1);
       if (warp == 0) BTRACE(6, tc);
       tc_fence_after();
-      uint32_t sv[64];
-      {
-        uint32_t (&s0)[32] = *reinterpret_cast<uint32_t (*)[32]>(&sv[0]);
-        uint32_t (&s1)[32] = *reinterpret_cast<uint32_t (*)[32]>(&sv[32]);
-        tmem_ld32(tl + C::kTmemS + 128 * buf + 64 * kh, s0);
-        tmem_ld32(tl + C::kTmemS + 128 * buf + 64 * kh + 32, s1);
-      }
+      uint32_t sv[32];
+      tmem_ld32(tl + C::kTmemS + 64 * buf + 32 * c, sv);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(sfree0 + 8 * buf);
       if (warp == 0) BTRACE(7, tc);
-      // the next tile's row inputs (and P) while this tile is processed
-      RowIter nx = it;
-      nx.advance();
-      const RowIn nxt = row_in(nx);
-      if (!kDvK) load_p(nxt);
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) {
+      for (int e2 = 0; e2 < 32; e2 += 2) {
         float v2[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int j = j0 + 64 * kh + c + e;
+          const int j = jk + e2 + e;
           const bool ok = cur.rv && cur.win && j < p.n_kv && (!p.causal || j <= cur.pos);
           if (kDvK) {
-            v2[e] = ok ? ex2(fmaf(__uint_as_float(sv[c + e]), p.sl2, -cur.lse2)) : 0.f;
+            v2[e] = ok ? ex2(fmaf(__uint_as_float(sv[e2 + e]), p.sl2, -cur.lse2)) : 0.f;
           } else {
-            const uint32_t w2 = pk[c >> 1];
+            const uint32_t w2 = pk[e2 >> 1];
             const float pv = e ? __uint_as_float(w2 & 0xFFFF0000u) : __uint_as_float(w2 << 16);
-            v2[e] = pv * (__uint_as_float(sv[c + e]) - cur.Dr);
+            v2[e] = pv * (__uint_as_float(sv[e2 + e]) - cur.Dr);
           }
         }
-        pk[c >> 1] = pack_bf16x2(v2[0], v2[1]);
+        pk[e2 >> 1] = pack_bf16x2(v2[0], v2[1]);
       }
       if (warp == 0) BTRACE(8, tc);
-      mbar_wait(bar(C::kBarPFree), (tc & 1) ^ 1);  // both CTAs' P buffers (and the staging) are free again
+      const int pb = tc & 1;
+      mbar_wait(bar(C::kBarPFree + pb), ((tc >> 1) & 1) ^ 1);  // buffer pb's last gradient UMMAs (tile tc - 2) ran
       if (warp == 0) BTRACE(9, tc);
-      // row of 128 B = 8 x 16-B units, SWIZZLE_128B: unit u at (u ^ row & 7)
+      // row of 128 B = 8 x 16-B units (this thread's: 4 c .. 4 c + 3), SWIZZLE_128B: unit u at (u ^ row & 7)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) st_shared_v4(pdst + ((u ^ sw) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      for (int u = 0; u < 4; ++u)
+        st_shared_v4(pdst + pb * pstride + (((4 * c + u) ^ sw) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2],
+                     pk[4 * u + 3]);
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive_local(bar(own ? C::kBarPLocal : C::kBarPStaged));
+      if (lane == 0) mbar_arrive_local(bar((own ? C::kBarPLocal : C::kBarPStaged) + pb));
       if (warp == 0) BTRACE(10, tc);
-      if (cur.ds) {  // P (dV kernel) or dS (dK kernel) of the row's 64 keys into the dS row buffer
+      if (prev_ds) {  // P (dV kernel) or dS (dK kernel) of the previous tile's row, 32 keys, to the dS row buffer
 #pragma unroll
-        for (int u = 0; u < 8; ++u) cur.ds[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        for (int u = 0; u < 4; ++u) prev_ds[u] = make_uint4(prev[4 * u], prev[4 * u + 1], prev[4 * u + 2], prev[4 * u + 3]);
       }
+      prev_ds = cur.ds;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) prev[u] = pk[u];
       it = nx;
       cur = nxt;
     }
+    if (prev_ds) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) prev_ds[u] = make_uint4(prev[4 * u], prev[4 * u + 1], prev[4 * u + 2], prev[4 * u + 3]);
+    }
     // ------------------------------------------------------------------ epilogue: TMEM lane = dim, column = key
     if (any) {
-      mbar_wait(bar(C::kBarPFree), (tc & 1) ^ 1);  // the last gradient commit (it precedes Acc) has landed
+      for (int u = tc - 2 < 0 ? 0 : tc - 2; u < tc; ++u)  // the last gradient commits (they precede Acc) landed
+        mbar_wait(bar(C::kBarPFree + (u & 1)), (u >> 1) & 1);
       mbar_wait(bar(C::kBarAcc), 0);
       tc_fence_after();
     }
@@ -1223,17 +1252,17 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       for (int hf = 0; hf < 2; ++hf) {
         uint32_t v[32];
         if (any) {
-          tmem_ld32(tl + C::kTmemAcc + 128 * g + 64 * kh + 32 * hf, v);
+          tmem_ld32(tl + C::kTmemAcc + 128 * g + 64 * c + 32 * hf, v);
           tmem_wait_ld();
         } else {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) v[c] = 0u;
+          for (int e = 0; e < 32; ++e) v[e] = 0u;
         }
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int j = j0 + 64 * kh + 32 * hf + c;
+        for (int e = 0; e < 32; ++e) {
+          const int j = j0 + 64 * c + 32 * hf + e;
           if (j >= p.n_kv) continue;
-          const float x = __uint_as_float(v[c]) * sc;
+          const float x = __uint_as_float(v[e]) * sc;
           if (split) {  // partials in the 32-key tile layout of the sink reduce: [B][n_sink][nsplit][32][1088]
             const int t32 = j >> 5, kl = j & 31;
             p.part[((((int64_t)bi * p.n_sink + t32) * p.nsplit + blockIdx.y) * kKeys + kl) * kDkv + (kDvK ? kDqk : 0) + dim] = x;
@@ -1535,7 +1564,10 @@ static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, fl
   if (!encode_4d_chunks(&p.q_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 2) ||
       !encode_4d_chunks(&p.o_map, dout, kDv, rows, a.batch, a.o_sh, a.o_sb, kRows, 2) ||
       !encode_4d_chunks(&p.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, 64, 9) ||
-      !encode_4d_chunks(&pk.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, 64, 8))
+      !encode_4d_chunks(&pk.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, 64, 8) ||
+      !encode_4d_chunks(&p.q4_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kPHalf, 4) ||
+      !encode_4d_chunks(&p.q1_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kPHalf, 1) ||
+      !encode_4d_chunks(&p.o4_map, dout, kDv, rows, a.batch, a.o_sh, a.o_sb, kPHalf, 4))
     return cudaErrorInvalidValue;
   p.lse = a.lse;
   p.D = D;
