@@ -501,9 +501,11 @@ def extra_rows(args, q, kv, o, flush, peaks):
     out["backward_ssa_8k"] = {
         "ms": bw_ms, "tflops": bw_flop / (bw_ms * 1e-3) / 1e12,
         "frac_tensor": bw_flop / (bw_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
-        "kernel": "tcgen05 (attn_bwd_tc.cu: D; 64-key dV kernel (dV^T in TMEM, P into the dS rows) and dK kernel "
-                  "(P from the dS rows, dK^T in TMEM, dS rows); dQ = dS K GEMM; sink tiles split over row ranges + fixed-order reduce); the 32-key "
-                  "one-pass key kernel 6.1 ms, warp-MMA 22 ms, FFMA 492 ms before it",
+        "kernel": "tcgen05 (attn_bwd_tc.cu: D beside the dV kernel; 128-key CTA-pair dV kernel (cta_group::2, S three "
+                  "row tiles ahead, P halves swapped by bulk DSMEM copies, dV^T in TMEM, P into the dS rows) and dK kernel "
+                  "(P from the dS rows, dK^T in TMEM, dS rows); dQ = dS K GEMM; sink tiles split by query blocks + "
+                  "fixed-order reduce); the 64-key kernels 4.25 ms, the 32-key one-pass key kernel 6.1 ms, warp-MMA 22 ms, "
+                  "FFMA 492 ms before it",
         "algorithmic_flop": bw_flop}
     del of, osp, dh, oh
     # non-absorbed (MHA-form) SSA prefill: per-head K/V (192 / 128) at the headline's 32K

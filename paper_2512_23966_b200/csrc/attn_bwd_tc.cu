@@ -943,7 +943,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
     prefetch_tmap(&p.o_map);
     prefetch_tmap(&p.k_map);
     prefetch_tmap(kDvK ? &p.q4_map : &p.o4_map);
-    if (kDvK) prefetch_tmap(&p.q1_map);
+    prefetch_tmap(&p.q1_map);
   }
   if (warp == kPMma) tmem_alloc<2>(smem_u32(tmem_ptr), 512);
   tc_fence_before();
@@ -963,11 +963,12 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       }
       __syncwarp();
       uint32_t slot = 0, ph = 0;
-      auto load = [&](const CUtensorMap* m, int row, int chunk, uint32_t bytes) {
+      // tx: the bytes both CTAs load into this slot; mine: whether this CTA loads (m, row, chunk)
+      auto load = [&](const CUtensorMap* m, int row, int chunk, uint32_t tx, bool mine = true) {
         mbar_wait(bar(C::kBarEmpty + slot), ph ^ 1);
         if (elect_one()) {
-          if (rank == 0) mbar_arrive_expect_tx(bar(C::kBarFull + slot), 2 * bytes);
-          tma_load_4d_pair(sbase + C::kOffRing + slot * kPairBytes, m, 0, row, chunk, bi, full_l + 8 * slot, pol);
+          if (rank == 0) mbar_arrive_expect_tx(bar(C::kBarFull + slot), tx);
+          if (mine) tma_load_4d_pair(sbase + C::kOffRing + slot * kPairBytes, m, 0, row, chunk, bi, full_l + 8 * slot, pol);
         }
         __syncwarp();
         if (++slot == C::kStages) {
@@ -980,16 +981,19 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       auto load_first = [&](int rb) {
         const int r = rb + kPHalf * (int)rank;
         if (kDvK) {
-          load(&p.q4_map, r, 0, kPairBytes);
-          load(&p.q4_map, r, 4, kPairBytes);
-          load(&p.q1_map, r, 8, kPairBytes / 4);
+          load(&p.q4_map, r, 0, 2 * kPairBytes);
+          load(&p.q4_map, r, 4, 2 * kPairBytes);
+          load(&p.q1_map, r, 8, 2 * kPairBytes / 4);
         } else {
-          load(&p.o4_map, r, 0, kPairBytes);
-          load(&p.o4_map, r, 4, kPairBytes);
+          load(&p.o4_map, r, 0, 2 * kPairBytes);
+          load(&p.o4_map, r, 4, 2 * kPairBytes);
         }
       };
       auto load_grad = [&](int rb) {
-        for (int g = 0; g < C::kGroups; ++g) load(kDvK ? &p.o_map : &p.q_map, rb, 2 * (2 * g + (int)rank), kPairBytes);
+        for (int g = 0; g < 2; ++g) load(kDvK ? &p.o_map : &p.q_map, rb, 2 * (2 * g + (int)rank), 2 * kPairBytes);
+        // dK^T's third group, dims 512..: CTA 0 stages chunk 8 alone ([1 chunk][128 rows], p.q1_map of the dK
+        // kernel), CTA 1 nothing; the UMMA rows they leave stale (dims 576..) are never stored
+        if (!kDvK) load(&p.q1_map, rb, 8, kPairBytes / 2, rank == 0);
       };
       RowIter ia = it;
       for (int i = 0; i < C::kAhead && ia.valid(); ++i) {
@@ -1601,6 +1605,8 @@ static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, fl
   pk = p;
   pk.k_map = k8;
   pk.trace = g_bwd_trace_mode == kPairDk ? g_bwd_trace : nullptr;
+  // the dK kernel's q1 box: [1 chunk][128 rows] (dK^T's third dim group)
+  if (!encode_4d_chunks(&pk.q1_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 1)) return cudaErrorInvalidValue;
   const int64_t kt = (a.n_kv + kPKeys - 1) / kPKeys;
   const bool use_part = a.sparse && nsplit > 1;
   const dim3 grid((unsigned)(2 * a.batch * kt), use_part ? nsplit : 1);
