@@ -825,9 +825,9 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
 //     dS  = P (dP - D) (P read back from the dS row buffer), into the dS row buffer and, split by keys as above,
 //           into the two CTAs' dS buffers
 //     dK^T [576 x 128] += Q^T dS            three M256 N128 groups (dims 512.. of the third: CTA 0 stages
-//                                           chunk 8 and a zero-filled chunk 9, CTA 1 two zero-filled chunks)
+//                                           chunk 8 only, CTA 1 nothing; the stale rows are never stored)
 // Per SM and 128 x 128 (row, key) pairs the dV kernel moves 136 KB of Q / dO (the 64-key kernel: 576 KB) and
-// the dK kernel 160 KB (64-key: 588 KB). TMEM per CTA: dV kernel S 4 x 64 + dV^T 2 x 128 columns; dK kernel
+// the dK kernel 144 KB (64-key: 588 KB). TMEM per CTA: dV kernel S 4 x 64 + dV^T 2 x 128 columns; dK kernel
 // dK^T 3 x 128 + dP 2 x 64. SMEM: ring 3 x 32 KB, K tile 72 KB (dV: 9 chunks) or 64 KB (dK: V's 8), P / dS
 // 2 x 16 KB, staging 2 x 8 KB. Warps 0-7 P / dS and the epilogue (warp w: TMEM lane quarter w % 4, column half w / 4),
 // warp 8 TMA, warp 9 UMMA issue (leader) and TMEM allocation, warp 10 the DSMEM copy.
