@@ -129,7 +129,15 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = p.heads;
   const int ktiles = (p.n_kv + kKeys - 1) / kKeys;
-  const int bi = blockIdx.x / ktiles, tile = blockIdx.x - bi * ktiles, j0 = tile * kKeys;
+  // blocks of a batch entry: the sink tiles' row splits first (as long as a full local tile: they must not
+  // start late), then one per local tile
+  const int nst = p.sparse && p.nsplit > 1 ? (int)(((int64_t)p.s * p.b + kKeys - 1) / kKeys) : 0;
+  const int ns = nst < ktiles ? nst : ktiles;
+  const int units = ns * p.nsplit + (ktiles - ns);
+  const int bi = (int)blockIdx.x / units, u = (int)blockIdx.x - bi * units;
+  const int tile = u < ns * p.nsplit ? u / p.nsplit : ns + (u - ns * p.nsplit);
+  const int ys = u < ns * p.nsplit ? u - tile * p.nsplit : 0;  // row split of a sink tile
+  const int j0 = tile * kKeys;
   // rows attending keys [j0, j0 + 32): positions [p0, p1) (as in attn_bwd_mma.cu)
   int p0 = p.causal ? j0 : 0, p1 = p.q_start + p.n_q;
   const int kb = j0 / p.b;
@@ -149,7 +157,7 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
     // hit the rows the local tiles stream at the same step)
     if (p1 > p0) {
       const int ma = p0 / p.b, nb = (p1 - 1) / p.b - ma + 1, cb = (nb + p.nsplit - 1) / p.nsplit;
-      const int a = (ma + (int)blockIdx.y * cb) * p.b, e = a + cb * p.b;
+      const int a = (ma + ys * cb) * p.b, e = a + cb * p.b;
       if (a > p0) p0 = a;
       if (e < p1) p1 = e;
     }
@@ -158,8 +166,6 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
       R0 = (p0 - p.q_start) * H;
       R1 = (p1 - p.q_start) * H;
     }
-  } else if (blockIdx.y > 0) {
-    return;
   }
   RowIter it;
   it.L = p.sparse && (split || kb >= p.s) ? p.l : 1;
@@ -414,7 +420,7 @@ __global__ void __launch_bounds__(256, 1) bwd_dkdv_tc_kernel(const __grid_consta
         if (j >= p.n_kv) continue;
         const float x = __uint_as_float(v[c]) * sc;
         if (split)
-          p.part[((((int64_t)bi * p.n_sink + tile) * p.nsplit + blockIdx.y) * kKeys + c) * kDkv + (isk ? 0 : kDqk) + dim] = x;
+          p.part[((((int64_t)bi * p.n_sink + tile) * p.nsplit + ys) * kKeys + c) * kDkv + (isk ? 0 : kDqk) + dim] = x;
         else if (isk)
           p.dk[((int64_t)bi * p.n_kv + j) * kDqk + dim] = x;
         else
@@ -475,7 +481,15 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = p.heads;
   const int ktiles = (p.n_kv + k64Keys - 1) / k64Keys;
-  const int bi = blockIdx.x / ktiles, tile = blockIdx.x - bi * ktiles, j0 = tile * k64Keys;
+  // blocks of a batch entry: the sink tiles' row splits first (as long as a full local tile: they must not
+  // start late), then one per local tile
+  const int nst = p.sparse && p.nsplit > 1 ? (int)(((int64_t)p.s * p.b + k64Keys - 1) / k64Keys) : 0;
+  const int ns = nst < ktiles ? nst : ktiles;
+  const int units = ns * p.nsplit + (ktiles - ns);
+  const int bi = (int)blockIdx.x / units, u = (int)blockIdx.x - bi * units;
+  const int tile = u < ns * p.nsplit ? u / p.nsplit : ns + (u - ns * p.nsplit);
+  const int ys = u < ns * p.nsplit ? u - tile * p.nsplit : 0;  // row split of a sink tile
+  const int j0 = tile * k64Keys;
   // rows attending keys [j0, j0 + 64) (b % 64 == 0: the tile lies in one block)
   int p0 = p.causal ? j0 : 0, p1 = p.q_start + p.n_q;
   const int kb = j0 / p.b;
@@ -495,7 +509,7 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
     // hit the rows the local tiles stream at the same step)
     if (p1 > p0) {
       const int ma = p0 / p.b, nb = (p1 - 1) / p.b - ma + 1, cb = (nb + p.nsplit - 1) / p.nsplit;
-      const int a = (ma + (int)blockIdx.y * cb) * p.b, e = a + cb * p.b;
+      const int a = (ma + ys * cb) * p.b, e = a + cb * p.b;
       if (a > p0) p0 = a;
       if (e < p1) p1 = e;
     }
@@ -504,8 +518,6 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
       R0 = (p0 - p.q_start) * H;
       R1 = (p1 - p.q_start) * H;
     }
-  } else if (blockIdx.y > 0) {
-    return;
   }
   RowIter it;
   it.L = p.sparse && (split || kb >= p.s) ? p.l : 1;
@@ -785,7 +797,7 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
           const float x = __uint_as_float(v[c]) * sc;
           if (split) {  // partials in the 32-key tile layout of the sink reduce: [B][n_sink][nsplit][32][1088]
             const int t32 = j >> 5, kl = j & 31;
-            p.part[((((int64_t)bi * p.n_sink + t32) * p.nsplit + blockIdx.y) * kKeys + kl) * kDkv + (kIsDv ? kDqk : 0) + dim] = x;
+            p.part[((((int64_t)bi * p.n_sink + t32) * p.nsplit + ys) * kKeys + kl) * kDkv + (kIsDv ? kDqk : 0) + dim] = x;
           } else if (kIsDv) {
             p.dv[((int64_t)bi * p.n_kv + j) * kDv + dim] = x;
           } else {
@@ -862,7 +874,7 @@ static_assert(PairCfg<kPairDv>::kSmem <= 232448 && PairCfg<kPairDk>::kSmem <= 23
 // clock64 timeline: trace[(slot * 2 + rank) * 64 + tile] for tiles < 64 of pair cluster trace_cluster
 #define BTRACE(slot, idx)                                                                                   \
   do {                                                                                                      \
-    if (p.trace && pc == p.trace_cluster && blockIdx.y == 0 && (idx) < 64 && (threadIdx.x & 31) == 0)       \
+    if (p.trace && pc == p.trace_cluster && (idx) < 64 && (threadIdx.x & 31) == 0)                          \
       p.trace[((slot) * 2 + rank) * 64 + (idx)] = clock64();                                                \
   } while (0)
 
@@ -879,8 +891,15 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
   const uint32_t rank = cluster_ctarank(), partner = rank ^ 1u;
   const int H = p.heads;
   const int ktiles = (p.n_kv + kPKeys - 1) / kPKeys;
+  // clusters of a batch entry: the sink tiles' row splits first (they are as long as a full local tile and must
+  // not start late), then one per local tile
+  const int ns = p.sparse && p.nsplit > 1 ? (p.s < ktiles ? p.s : ktiles) : 0;
+  const int units = ns * p.nsplit + (ktiles - ns);
   const int pc = (int)(blockIdx.x >> 1);
-  const int bi = pc / ktiles, tile = pc - bi * ktiles, j0 = tile * kPKeys;
+  const int bi = pc / units, u = pc - bi * units;
+  const int tile = u < ns * p.nsplit ? u / p.nsplit : ns + (u - ns * p.nsplit);
+  const int ys = u < ns * p.nsplit ? u - tile * p.nsplit : 0;  // row split of a sink tile
+  const int j0 = tile * kPKeys;
   // rows attending keys [j0, j0 + 128) (b == 128: the tile is one block)
   int p0 = p.causal ? j0 : 0, p1 = p.q_start + p.n_q;
   const int kb = j0 / p.b;
@@ -893,12 +912,10 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
   if (split) {  // sink tile: rows split by whole query blocks, walked in the local tiles' rotation
     if (p1 > p0) {
       const int ma = p0 / p.b, nb = (p1 - 1) / p.b - ma + 1, cb = (nb + p.nsplit - 1) / p.nsplit;
-      const int a = (ma + (int)blockIdx.y * cb) * p.b, e = a + cb * p.b;
+      const int a = (ma + ys * cb) * p.b, e = a + cb * p.b;
       if (a > p0) p0 = a;
       if (e < p1) p1 = e;
     }
-  } else if (blockIdx.y > 0) {
-    return;  // both CTAs of the pair
   }
   RowIter it;
   it.L = p.sparse && (split || kb >= p.s) ? p.l : 1;
@@ -913,6 +930,13 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
   it.b = p.b;
   it.start();
   const bool any = it.valid();
+  // debug (trace_cluster < 0): globaltimer at start / end of every cluster, [pc][2] (rank 0, thread 0)
+  const bool gtrace = p.trace && p.trace_cluster < 0 && rank == 0 && threadIdx.x == 0;
+  if (gtrace) {
+    uint64_t g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    p.trace[(int64_t)pc * 2] = g;
+  }
 
   auto bar = [&](int i) { return sbase + C::kOffBar + 8 * i; };
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::kOffTmemPtr);
@@ -1269,7 +1293,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
           const float x = __uint_as_float(v[e]) * sc;
           if (split) {  // partials in the 32-key tile layout of the sink reduce: [B][n_sink][nsplit][32][1088]
             const int t32 = j >> 5, kl = j & 31;
-            p.part[((((int64_t)bi * p.n_sink + t32) * p.nsplit + blockIdx.y) * kKeys + kl) * kDkv + (kDvK ? kDqk : 0) + dim] = x;
+            p.part[((((int64_t)bi * p.n_sink + t32) * p.nsplit + ys) * kKeys + kl) * kDkv + (kDvK ? kDqk : 0) + dim] = x;
           } else if (kDvK) {
             p.dv[((int64_t)bi * p.n_kv + j) * kDv + dim] = x;
           } else {
@@ -1282,6 +1306,11 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
   tc_fence_before();
   __syncthreads();
   cluster_sync();
+  if (gtrace) {
+    uint64_t g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    p.trace[(int64_t)pc * 2 + 1] = g;
+  }
   if (warp == kPMma) {
     tc_fence_after();
     tmem_dealloc<2>(tmem, 512);
@@ -1545,8 +1574,9 @@ cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk
   cudaError_t e = cudaFuncSetAttribute(bwd_dkdv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   if (e != cudaSuccess) return e;
   const int64_t kt = (a.n_kv + kKeys - 1) / kKeys;
-  const bool use_part = a.sparse && nsplit > 1;
-  bwd_dkdv_tc_kernel<<<dim3((unsigned)(a.batch * kt), use_part ? nsplit : 1), 256, kSmem, st>>>(p);
+  const int64_t nst = a.sparse && nsplit > 1 ? ((int64_t)a.s * a.b + kKeys - 1) / kKeys : 0;
+  const int64_t ns = nst < kt ? nst : kt;  // sink tiles, split over rows
+  bwd_dkdv_tc_kernel<<<(unsigned)(a.batch * (ns * nsplit + kt - ns)), 256, kSmem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }
@@ -1608,8 +1638,8 @@ static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, fl
   // the dK kernel's q1 box: [1 chunk][128 rows] (dK^T's third dim group)
   if (!encode_4d_chunks(&pk.q1_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 1)) return cudaErrorInvalidValue;
   const int64_t kt = (a.n_kv + kPKeys - 1) / kPKeys;
-  const bool use_part = a.sparse && nsplit > 1;
-  const dim3 grid((unsigned)(2 * a.batch * kt), use_part ? nsplit : 1);
+  const int64_t ns = a.sparse && nsplit > 1 ? (a.s < kt ? a.s : kt) : 0;  // sink tiles, split over rows
+  const dim3 grid((unsigned)(2 * a.batch * (ns * nsplit + kt - ns)));
   cudaError_t e = cudaFuncSetAttribute(bwd_pair_tc_kernel<kPairDv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<kPairDv>::kSmem);
   if (e == cudaSuccess)
@@ -1663,8 +1693,9 @@ cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* d
     p.h_m = (uint32_t)(((1ull << p.h_p) + a.heads - 1) / a.heads);
   }
   const int64_t kt = (a.n_kv + k64Keys - 1) / k64Keys;
-  const bool use_part = a.sparse && nsplit > 1;
-  const dim3 grid((unsigned)(a.batch * kt), use_part ? nsplit : 1);
+  const int64_t nst = a.sparse && nsplit > 1 ? ((int64_t)a.s * a.b + k64Keys - 1) / k64Keys : 0;
+  const int64_t ns = nst < kt ? nst : kt;  // sink tiles, split over rows
+  const dim3 grid((unsigned)(a.batch * (ns * nsplit + kt - ns)));
   cudaError_t e = cudaFuncSetAttribute(bwd_key64_tc_kernel<kDvOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64Smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(bwd_key64_tc_kernel<kDkOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64Smem);
