@@ -1326,7 +1326,9 @@ constexpr int kQdN = 192, kQdStages = 4;
 constexpr int kQdA = kRows * 128;          // [128 rows][64 slots] bf16, SW128
 constexpr int kQdB = 3 * 64 * 128;         // [3 chunks][64 keys][64 dims], SW128
 constexpr int kQdStage = kQdA + kQdB;      // 40 KB
-constexpr int kQdOffBar = kQdStages * kQdStage;
+constexpr int kQdOffSt = kQdStages * kQdStage;       // epilogue staging: 4 warps x 2 x [32 rows][32 fp32], SW128
+constexpr int kQdStBytes = 32 * 128;
+constexpr int kQdOffBar = kQdOffSt + 4 * 2 * kQdStBytes;
 constexpr int kQdNumBars = 2 * kQdStages + 4;
 constexpr int kQdOffTmemPtr = kQdOffBar + 8 * kQdNumBars;
 constexpr int kQdSmem = kQdOffTmemPtr + 16 + 1024;
@@ -1334,6 +1336,7 @@ constexpr int kQdSmem = kQdOffTmemPtr + 16 + 1024;
 struct TcDqParams {
   CUtensorMap ds_map;  // 3-D {W slots, rows, B}, box {64, 128, 1}
   CUtensorMap k_map;   // 4-D {64, n_kv, 9, B}, box {64, 64, 3, 1}
+  CUtensorMap dq_map;  // 3-D fp32 {576, rows, B}, box {32, 32, 1}, SW128 (epilogue TMA stores)
   float* dq;
   int32_t rows, heads, n_kv, q_start, s, l, b, kv32, batch;
   float scale;
@@ -1404,6 +1407,7 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_tc_kernel(const __grid_constant
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.ds_map);
     prefetch_tmap(&p.k_map);
+    prefetch_tmap(&p.dq_map);
   }
   if (warp == 1) tmem_alloc<1>(smem_u32(tmem_ptr), 512);
   tc_fence_before();
@@ -1462,15 +1466,17 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_tc_kernel(const __grid_constant
       __syncwarp();
     }
   } else if (warp >= 4) {
+    // a row's 32 values per TMEM load into a swizzled [32 rows][32 fp32] staging block, then one TMA store of
+    // 32 full 128-B row pieces (per-thread row stores wrote half sectors and queued behind each other)
     const int q = warp - 4, row = 32 * q + lane;
-    int n = 0;
+    const uint32_t st0 = sbase + kQdOffSt + (uint32_t)q * 2 * kQdStBytes, sw = (uint32_t)(lane & 7);
+    int n = 0, k = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
       const Tile T = decode(t);
-      const int ab = n & 1, use = n >> 1, r = T.r0 + row;
+      const int ab = n & 1, use = n >> 1;
       mbar_wait(bar(kAccFull + ab), use & 1);
       tc_fence_after();
-      float* out = p.dq + ((int64_t)T.bi * p.rows + r) * kDqk + kQdN * T.slice;
-      for (int g = 0; g < kQdN / 32; ++g) {
+      for (int g = 0; g < kQdN / 32; ++g, ++k) {
         uint32_t v[32];
         if (T.nch > 0) {
           tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + kQdN * ab + 32 * g, v);
@@ -1479,18 +1485,30 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_tc_kernel(const __grid_constant
 #pragma unroll
           for (int c = 0; c < 32; ++c) v[c] = 0u;
         }
-        if (r < p.rows) {
+        if (g == kQdN / 32 - 1) {  // the accumulator is read: the next-but-one tile may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_local(bar(kAccFree + ab));
+        }
+        const uint32_t sb = st0 + (uint32_t)(k & 1) * kQdStBytes;
+        if (lane == 0) bulk_wait_group_read1();  // the store that last read this staging block is done
+        __syncwarp();
 #pragma unroll
-          for (int c = 0; c < 32; c += 4)
-            *reinterpret_cast<float4*>(out + 32 * g + c) =
-                make_float4(__uint_as_float(v[c]) * p.scale, __uint_as_float(v[c + 1]) * p.scale,
-                            __uint_as_float(v[c + 2]) * p.scale, __uint_as_float(v[c + 3]) * p.scale);
+        for (int u = 0; u < 8; ++u)
+          st_shared_v4(sb + lane * 128 + ((u ^ sw) << 4), __float_as_uint(__uint_as_float(v[4 * u]) * p.scale),
+                       __float_as_uint(__uint_as_float(v[4 * u + 1]) * p.scale),
+                       __float_as_uint(__uint_as_float(v[4 * u + 2]) * p.scale),
+                       __float_as_uint(__uint_as_float(v[4 * u + 3]) * p.scale));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {  // rows past p.rows are clipped by the tensor map
+          tma_store_3d(&p.dq_map, sb, kQdN * T.slice + 32 * g, T.r0 + 32 * q, T.bi);
+          bulk_commit_group();
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_local(bar(kAccFree + ab));
+      (void)row;
     }
+    if (lane == 0) bulk_wait_group0();
   }
   tc_fence_before();
   __syncthreads();
@@ -1743,7 +1761,8 @@ cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq
   const int W = (a.s + a.l) * a.b;
   const uint64_t rows = (uint64_t)a.n_q * a.heads;
   if (!encode_3d(&p.ds_map, ds, (uint64_t)W, rows, a.batch, W, (int64_t)rows * W, kRows) ||
-      !encode_4d_chunks(&p.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, 64, 3))
+      !encode_4d_chunks(&p.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, 64, 3) ||
+      !encode_3d_f32(&p.dq_map, dq, kDqk, rows, a.batch, kDqk, (int64_t)rows * kDqk, 32))
     return cudaErrorInvalidValue;
   p.dq = dq;
   p.rows = (int32_t)rows;

@@ -134,6 +134,8 @@ bool encode_3d(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint
 bool encode_5d_heads(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t heads, uint64_t batch,
                      int64_t row_stride_el, int64_t head_stride_el, int64_t batch_stride_el, uint32_t box_rows,
                      uint32_t box_chunks);
+bool encode_3d_f32(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t batch, int64_t row_stride_el,
+                   int64_t batch_stride_el, uint32_t box_rows);
 bool encode_4d_chunks(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t batch,
                       int64_t row_stride_el, int64_t batch_stride_el, uint32_t box_rows, uint32_t box_chunks);
 }  // namespace loza

@@ -37,6 +37,24 @@ bool encode_3d(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint
   return r == CUDA_SUCCESS;
 }
 
+// 3-D fp32 map {d (contiguous), rows, batch}, box {32, box_rows, 1} (128 B rows), 128B swizzle: the dQ
+// epilogue's TMA stores
+bool encode_3d_f32(CUtensorMap* m, const void* base, uint64_t d, uint64_t rows, uint64_t batch, int64_t row_stride_el,
+                   int64_t batch_stride_el, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc || d % 4 != 0) return false;
+  if (rows == 0) rows = 1;
+  if (batch == 0) batch = 1;
+  cuuint64_t dims[3] = {d, rows, batch};
+  cuuint64_t strides[2] = {(cuuint64_t)row_stride_el * 4, (cuuint64_t)(batch_stride_el > 0 ? batch_stride_el : rows * row_stride_el) * 4};
+  cuuint32_t box[3] = {32, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // 4-D bf16 view {64 (contiguous), rows, d/64 column chunks, batch} of a [batch, rows, d] tensor: one box
 // {64, box_rows, box_chunks, 1} fetches box_chunks adjacent 64-column chunks; in SMEM the chunks follow
 // each other (box_rows x 128 B each), i.e. the layout of box_chunks separate 3-D loads.
