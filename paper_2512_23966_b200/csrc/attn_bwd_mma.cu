@@ -740,7 +740,8 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
       e = launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st);
     }
     if (e != cudaSuccess) return e;
-    if ((e = launch_bwd_dq_tc(a, ds, dq, st)) != cudaSuccess) return e;
+    const bool pair_keys = key64 && knob(kKnobBackward) != 5 && backward_pair_eligible(a);
+    if ((e = launch_bwd_dq_tc(a, ds, dq, st, pair_keys)) != cudaSuccess) return e;
     if (use_part) {
       const int64_t n = (int64_t)a.batch * p.n_sink * kKKeys * (kDKV / 4);
       bwd_sink_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p);

@@ -1518,6 +1518,205 @@ __global__ void __launch_bounds__(256, 1) bwd_dq_tc_kernel(const __grid_constant
   }
 }
 
+// dQ = dS K on CTA pairs (cta_group::2), when the key side ran the 128-key pair kernels (every slot of the blocks
+// up to a row's own was written for every row of its block) and 256-row tiles stay in one query block:
+// a pair tile = 256 rows (CTA r: 128, the M half) x a 256-dim slice (CTA r stages 128 of the slice's dims, the
+// N half of B): M256 N256 K16 UMMAs (the third slice, dims 512..575, N128 with CTA 1's half out of range). Per
+// CTA and 64 slots: 16 KB of dS + 16 KB of K for 512 tensor cycles (the single-CTA M128 N192 kernel: 40 KB per
+// 384). Six 32 KB stages; the epilogue's TMA stores as in bwd_dq_tc_kernel.
+constexpr int kQpStages = 6;
+constexpr int kQpA = kRows * 128;          // [128 rows][64 slots] bf16, SW128
+constexpr int kQpB = 2 * 64 * 128;         // [2 chunks][64 keys][64 dims], SW128
+constexpr int kQpStage = kQpA + kQpB;      // 32 KB
+constexpr int kQpOffSt = kQpStages * kQpStage;
+constexpr int kQpOffBar = kQpOffSt + 4 * 2 * kQdStBytes;
+constexpr int kQpNumBars = 2 * kQpStages + 4;
+constexpr int kQpOffTmemPtr = kQpOffBar + 8 * kQpNumBars;
+constexpr int kQpSmem = kQpOffTmemPtr + 16 + 1024;
+static_assert(kQpSmem <= 232448, "smem");
+
+__global__ void __launch_bounds__(256, 1) __cluster_dims__(2, 1, 1) bwd_dq_pair_kernel(const __grid_constant__ TcDqParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sbase - sraw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int prt = (p.rows + 2 * kRows - 1) / (2 * kRows);  // pair row tiles per batch entry
+  const int ntiles = p.batch * prt * 3;
+  const int cid = (int)(blockIdx.x >> 1), ncl = (int)(gridDim.x >> 1);
+  struct Tile {
+    int bi, r0, slice, lbq, se, nsc, nch;
+  };
+  auto decode = [&](int t) {
+    Tile T;
+    T.slice = t % 3;
+    const int rest = t / 3;
+    T.bi = rest / prt;
+    T.r0 = (rest - T.bi * prt) * 2 * kRows;
+    const int t0 = (int)(((uint64_t)(uint32_t)T.r0 * p.h_m) >> p.h_p), QB = (p.q_start + t0) / p.b;
+    T.lbq = QB - p.l + 1 < p.s ? p.s : QB - p.l + 1;
+    T.se = (QB + 1 < p.s ? QB + 1 : p.s) * p.b;  // sink slots the rows' block can see
+    const int nl = QB >= T.lbq ? (QB + 1 - T.lbq) * p.b : 0;
+    T.nsc = (T.se + 63) / 64;
+    T.nch = T.nsc + nl / 64;
+    return T;
+  };
+  auto chunk = [&](const Tile& T, int c, int& slot, int& key) {
+    if (c < T.nsc) {
+      slot = key = 64 * c;
+    } else {
+      const int i = 64 * (c - T.nsc);
+      slot = p.s * p.b + i;
+      key = T.lbq * p.b + i;
+    }
+  };
+  // barriers: Full[kQpStages] (leader), Empty[kQpStages], AccFull[2], AccFree[2] (leader, 4 warps x 2 CTAs)
+  auto bar = [&](int i) { return sbase + kQpOffBar + 8 * i; };
+  const int kAccFull = 2 * kQpStages, kAccFree = kAccFull + 2;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + kQpOffTmemPtr);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kQpStages; ++i) {
+      mbar_init(bar(i), 1);
+      mbar_init(bar(kQpStages + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(kAccFull + i), 1);
+      mbar_init(bar(kAccFree + i), 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.ds_map);
+    prefetch_tmap(&p.k_map);
+    prefetch_tmap(&p.dq_map);
+  }
+  if (warp == 1) tmem_alloc<2>(smem_u32(tmem_ptr), 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA (each CTA: its rows, its dims)
+    const uint64_t pol = policy_evict_normal(), pol_k = policy_evict_last();
+    const uint32_t full_l = mapa(bar(0), 0);
+    uint32_t slot = 0, ph = 0;
+    for (int t = cid; t < ntiles; t += ncl) {
+      const Tile T = decode(t);
+      for (int c = 0; c < T.nch; ++c) {
+        int sl, key;
+        chunk(T, c, sl, key);
+        mbar_wait(bar(kQpStages + slot), ph ^ 1);
+        if (elect_one()) {
+          if (rank == 0) mbar_arrive_expect_tx(bar(slot), 2 * kQpStage);
+          const uint32_t dst = sbase + slot * kQpStage;
+          tma_load_3d_pair(dst, &p.ds_map, sl, T.r0 + kRows * (int)rank, T.bi, full_l + 8 * slot, pol);
+          tma_load_4d_pair(dst + kQpA, &p.k_map, 0, key, 4 * T.slice + 2 * (int)rank, T.bi, full_l + 8 * slot, pol_k);
+        }
+        __syncwarp();
+        if (++slot == kQpStages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    for (int i = 0; i < kQpStages; ++i) {  // drain: the last Empty commits land before this CTA exits
+      mbar_wait(bar(kQpStages + slot), ph ^ 1);
+      if (++slot == kQpStages) {
+        slot = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- UMMA issuer (leader)
+    if (rank == 0) {
+      constexpr uint32_t id256 = idesc_bf16_f32(256, 256, false, true), id128 = idesc_bf16_f32(256, 128, false, true);
+      uint32_t slot = 0, ph = 0;
+      int n = 0;
+      for (int t = cid; t < ntiles; t += ncl, ++n) {
+        const Tile T = decode(t);
+        const int ab = n & 1, use = n >> 1;
+        mbar_wait(bar(kAccFree + ab), (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t id = T.slice < 2 ? id256 : id128;
+        for (int c = 0; c < T.nch; ++c) {
+          const int nk = c < T.nsc && T.se - 64 * c < 64 ? (T.se - 64 * c) / 16 : 4;
+          mbar_wait(bar(slot), ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a = sbase + slot * kQpStage;
+            for (int k = 0; k < nk; ++k)
+              umma_bf16_pair(tmem + 256 * ab, sdesc_sw128(a + 32 * k, 16, 1024),
+                             sdesc_sw128(a + kQpA + 2048 * k, 8192, 1024), id, (c | k) != 0);
+            umma_commit_pair_mc(bar(kQpStages + slot), 3);
+          }
+          __syncwarp();
+          if (++slot == kQpStages) {
+            slot = 0;
+            ph ^= 1;
+          }
+        }
+        if (elect_one()) umma_commit_pair_mc(bar(kAccFull + ab), 3);
+        __syncwarp();
+      }
+      for (int u = n - 2 < 0 ? 0 : n - 2; u < n; ++u)  // the partner's last AccFree arrivals land before exit
+        mbar_wait(bar(kAccFree + (u & 1)), (u >> 1) & 1);
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue (thread = row, TMA stores)
+    const int q = warp - 4;
+    const uint32_t st0 = sbase + kQpOffSt + (uint32_t)q * 2 * kQdStBytes, sw = (uint32_t)(lane & 7);
+    const uint32_t afree0 = mapa(bar(kAccFree), 0);
+    int n = 0, k = 0;
+    for (int t = cid; t < ntiles; t += ncl, ++n) {
+      const Tile T = decode(t);
+      const int ab = n & 1, use = n >> 1;
+      mbar_wait(bar(kAccFull + ab), use & 1);
+      tc_fence_after();
+      const int ng = T.slice < 2 ? 8 : 2;  // 32-dim groups stored (the third slice: dims 512..575)
+      for (int g = 0; g < ng; ++g, ++k) {
+        uint32_t v[32];
+        if (T.nch > 0) {
+          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 256 * ab + 32 * g, v);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) v[c] = 0u;
+        }
+        if (g == ng - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(afree0 + 8 * ab);
+        }
+        const uint32_t sb = st0 + (uint32_t)(k & 1) * kQdStBytes;
+        if (lane == 0) bulk_wait_group_read1();
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          st_shared_v4(sb + lane * 128 + ((u ^ sw) << 4), __float_as_uint(__uint_as_float(v[4 * u]) * p.scale),
+                       __float_as_uint(__uint_as_float(v[4 * u + 1]) * p.scale),
+                       __float_as_uint(__uint_as_float(v[4 * u + 2]) * p.scale),
+                       __float_as_uint(__uint_as_float(v[4 * u + 3]) * p.scale));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&p.dq_map, sb, 256 * T.slice + 32 * g, T.r0 + kRows * (int)rank + 32 * q, T.bi);
+          bulk_commit_group();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_group0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<2>(tmem, 512);
+  }
+}
+
 // D_r = dO_r . O_r (fp32), one warp per row (bf16 O and dO with o's strides, d_v 512)
 __global__ void __launch_bounds__(256) bwd_D_kernel(const uint16_t* o, const uint16_t* dout, float* D, int32_t rows,
                                                    int32_t batch, int64_t o_sb, int64_t o_st, int64_t o_sh,
@@ -1599,6 +1798,8 @@ cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk
   return cudaGetLastError();
 }
 
+bool backward_pair_eligible(const AttnProblem& a) { return a.sparse && a.b == kPKeys; }
+
 // 64-key tiles (two kernels, dV then dK): the tile must lie in one block (b % 64 == 0) when sparse
 bool backward_key64_eligible(const AttnProblem& a) { return !a.sparse || a.b % k64Keys == 0; }
 
@@ -1675,7 +1876,7 @@ static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, fl
 cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
                                 float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st,
                                 cudaEvent_t d_ready, bool allow_pair) {
-  if (allow_pair && ds && a.sparse && a.b == kPKeys)
+  if (allow_pair && ds && backward_pair_eligible(a))
     return launch_bwd_pair_tc(a, dout, dk, dv, D, part, ds, nsplit, n_sink, st, d_ready);
   TcBwdParams p;
   const auto& kv = a.kv.seg[0];
@@ -1755,13 +1956,16 @@ cudaError_t launch_bwd_D(const AttnProblem& a, const void* dout, float* D, cudaS
   return cudaGetLastError();
 }
 
-cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq, cudaStream_t st) {
+cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq, cudaStream_t st, bool pair_keys) {
   TcDqParams p;
   const auto& kv = a.kv.seg[0];
   const int W = (a.s + a.l) * a.b;
   const uint64_t rows = (uint64_t)a.n_q * a.heads;
+  // the pair GEMM needs every slot of a row's visible blocks written (the 128-key pair key kernels) and 256-row
+  // tiles inside one query block
+  const bool pair = pair_keys && ((int64_t)a.b * a.heads) % (2 * kRows) == 0;
   if (!encode_3d(&p.ds_map, ds, (uint64_t)W, rows, a.batch, W, (int64_t)rows * W, kRows) ||
-      !encode_4d_chunks(&p.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, 64, 3) ||
+      !encode_4d_chunks(&p.k_map, kv.k, kDqk, (uint64_t)a.n_kv, a.batch, kv.k_st, kv.k_sb, 64, pair ? 2 : 3) ||
       !encode_3d_f32(&p.dq_map, dq, kDqk, rows, a.batch, kDqk, (int64_t)rows * kDqk, 32))
     return cudaErrorInvalidValue;
   p.dq = dq;
@@ -1781,14 +1985,25 @@ cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq
     p.h_p = 31 + l;
     p.h_m = (uint32_t)(((1ull << p.h_p) + a.heads - 1) / a.heads);
   }
-  cudaError_t e = cudaFuncSetAttribute(bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kQdSmem);
-  if (e != cudaSuccess) return e;
-  const int64_t rt = ((int64_t)rows + kRows - 1) / kRows, tiles = a.batch * rt * 3;
   int sms = 148;
   {
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  cudaError_t e;
+  if (pair) {
+    if ((e = cudaFuncSetAttribute(bwd_dq_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kQpSmem)) !=
+        cudaSuccess)
+      return e;
+    const int64_t prt = ((int64_t)rows + 2 * kRows - 1) / (2 * kRows), tiles = a.batch * prt * 3;
+    const int64_t ncl = tiles < sms / 2 ? tiles : sms / 2;
+    bwd_dq_pair_kernel<<<(unsigned)(2 * ncl), 256, kQpSmem, st>>>(p);
+    count_launch();
+    return cudaGetLastError();
+  }
+  e = cudaFuncSetAttribute(bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kQdSmem);
+  if (e != cudaSuccess) return e;
+  const int64_t rt = ((int64_t)rows + kRows - 1) / kRows, tiles = a.batch * rt * 3;
   bwd_dq_tc_kernel<<<(unsigned)(tiles < sms ? tiles : sms), 256, kQdSmem, st>>>(p);
   count_launch();
   return cudaGetLastError();

@@ -103,7 +103,11 @@ cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* d
                                 cudaEvent_t d_ready = nullptr, bool allow_pair = true);
 size_t backward_ds_bytes(const AttnProblem& a);
 cudaError_t launch_bwd_D(const AttnProblem& a, const void* dout, float* D, cudaStream_t st);
-cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq, cudaStream_t st);
+// pair_keys: the key side ran the 128-key CTA-pair kernels (backward_pair_eligible), which write every slot of a
+// row's visible blocks; dQ then runs on CTA pairs too when 256-row tiles stay inside one query block
+cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq, cudaStream_t st, bool pair_keys);
+// SSA with b == 128: the 128-key CTA-pair key kernels can take it (with the dS row buffer)
+bool backward_pair_eligible(const AttnProblem& a);
 cudaError_t launch_attn_backward(const AttnProblem& a, const void* dout, float* dq, float* dk, float* dv, void* ws,
                                  cudaStream_t st);
 cudaError_t launch_ring_append(const void* rows, int64_t r_sb, int64_t r_st, int32_t m, const int32_t* pos0,
