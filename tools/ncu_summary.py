@@ -1,36 +1,32 @@
-"""Summarise an .ncu-rep into profiles/<name>.raw.txt (selected raw metrics per launch) and
-profiles/<name>.details.txt (the details page): python tools/ncu_summary.py REP NAME"""
+"""Summarise an .ncu-rep: key raw metrics per kernel and the top SASS stall lines.
+python tools/ncu_summary.py REP OUT.txt "command line" """
 import csv
-import io
 import subprocess
 import sys
 
-rep, name = sys.argv[1], sys.argv[2]
-KEYS = ["Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
-        "l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "launch__block_size", "launch__grid_size",
-        "launch__cluster_dim_x", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
-        "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second",
-        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
-        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
-        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
-        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
-        "lts__t_bytes.sum"]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(raw)))
-hdr, units = rows[0], rows[1]
-with open(f"profiles/{name}.raw.txt", "w") as f:
-    for li, vals in enumerate(rows[2:]):
-        f.write(f"# launch {li}\n")
-        for k in KEYS:
-            for h, u, v in zip(hdr, units, vals):
-                if h == k or h.endswith("." + k) or (k == "Kernel Name" and h == "Kernel Name"):
-                    f.write(f"{k} = {v} {u}\n")
-                    break
-det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(det)))
-hdr = rows[0]
-si, mi, vi, ui = hdr.index("Section Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-with open(f"profiles/{name}.details.txt", "w") as f:
-    for r in rows[1:]:
-        f.write(f"{r[si]:<32s} | {r[mi]:<40s} | {r[vi]:>14s} {r[ui]}\n")
-print(open(f"profiles/{name}.raw.txt").read())
+rep, out, cmd = sys.argv[1], sys.argv[2], sys.argv[3]
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__m_xbar2l1tex_read_bytes.sum",
+        "lts__t_sector_hit_rate.pct", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__cycles_active.avg", "gpc__cycles_elapsed.max", "launch__registers_per_thread", "launch__grid_size"]
+raw = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                                     text=True).stdout.splitlines()))
+lines = [f"# {cmd}"]
+h, units = raw[0], raw[1]
+for row in raw[2:]:
+    lines.append(row[h.index("Kernel Name")])
+    lines += [f"  {k} = {row[h.index(k)]} {units[h.index(k)]}" for k in KEYS if k in h]
+src = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True,
+                                     text=True).stdout.splitlines()))
+if len(src) > 2:
+    sh, data = src[1], src[2:]
+    si = sh.index("Warp Stall Sampling (All Samples)")
+    tot = sum(int(r[si]) for r in data if r[si].isdigit()) or 1
+    cols = [c for c in sh if c.startswith("stall_") and "Not Issued" not in c]
+    lines.append("top SASS lines by warp stall samples (first kernel of the report):")
+    for r in sorted(data, key=lambda r: -int(r[si]) if r[si].isdigit() else 0)[:10]:
+        st = sorted(((c, int(r[sh.index(c)])) for c in cols if r[sh.index(c)].isdigit()), key=lambda x: -x[1])[:2]
+        lines.append(f"  {int(r[si]) / tot * 100:5.1f}%  {r[1].strip()[:64]:64s} {st}")
+open(out, "w").write("\n".join(lines) + "\n")
+print("\n".join(lines))
