@@ -621,6 +621,7 @@ __global__ void __launch_bounds__(256) bwd_sink_reduce_kernel(MP p) {
 
 int sink_splits(const AttnProblem& a) {
   if (!a.sparse || a.s == 0 || a.n_kv == 0) return 1;  // no sink tiles: nothing to split
+  if (backward_pair_eligible(a)) return backward_pair_splits(a).nsplit;  // pieces as long as the local tiles' 
   const int64_t win = (int64_t)a.l * a.b;
   int64_t n = (a.n_q + win - 1) / win;
   return (int)(n < 1 ? 1 : n > 64 ? 64 : n);
@@ -733,8 +734,11 @@ cudaError_t launch_attn_backward_mma(const AttnProblem& a, const void* dout, flo
       if ((e = cudaStreamWaitEvent(sc->side, sc->fork, 0)) != cudaSuccess) return e;
       if ((e = launch_bwd_D(a, dout, D, sc->side)) != cudaSuccess) return e;
       if ((e = cudaEventRecord(sc->join, sc->side)) != cudaSuccess) return e;
+      // the local-tile row-split partials follow the sink partials in the workspace
+      float* part_local = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(part) +
+                                                   (backward_mma_part_bytes(a) + 255) / 256 * 256);
       e = launch_bwd_key64_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st, sc->join,
-                              knob(kKnobBackward) != 5);
+                              knob(kKnobBackward) != 5, part_local);
     } else {
       if ((e = launch_bwd_D(a, dout, D, st)) != cudaSuccess) return e;
       e = launch_bwd_dkdv_tc(a, dout, dk, dv, D, part, ds, p.nsplit, p.n_sink, st);

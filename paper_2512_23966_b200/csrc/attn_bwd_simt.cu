@@ -629,7 +629,10 @@ __global__ void __launch_bounds__(256) bwd_keys_async_kernel(BwdParams p) {
 static size_t d_bytes(const AttnProblem& a) {
   return (sizeof(float) * (size_t)a.batch * a.n_q * a.heads + 255) / 256 * 256;
 }
-static size_t part_bytes(const AttnProblem& a) { return (backward_mma_part_bytes(a) + 255) / 256 * 256; }
+// sink-tile partials, then the pair key kernels' local-tile row-split partials (short sequences)
+static size_t part_bytes(const AttnProblem& a) {
+  return (backward_mma_part_bytes(a) + 255) / 256 * 256 + (backward_local_part_bytes(a) + 255) / 256 * 256;
+}
 // D, then (tensor-core path, SSA) the sink-tile partials and the dS rows (attn_bwd_mma.cu / attn_bwd_tc.cu)
 // (the dS rows only when the tcgen05 dS path can run: bf16 MLA shape, V aliasing K, packed rows)
 size_t backward_ws_bytes(const AttnProblem& a) {

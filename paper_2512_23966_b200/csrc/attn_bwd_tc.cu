@@ -55,11 +55,13 @@ struct TcBwdParams {
   float* dk;
   float* dv;
   float* part;
+  float* part_local;  // pair kernels with local row splits: [B][kt - ns][lsplit][128][1088]
   uint16_t* ds;  // SSA: dS rows [B][n_q*H][(s+l)*b] bf16 (slot = sink key, then the row's local window), or NULL
   int32_t batch, n_q, heads, n_kv, q_start;
   float scale, sl2;
   int32_t sparse, causal, s, l, b;
   int32_t nsplit, n_sink;
+  int32_t lsplit;  // pair kernels: row splits of every local tile (1: none)
   uint32_t h_m, h_p;
   unsigned long long* trace;  // debug timeline of pair cluster trace_cluster (pair kernels; NULL in production)
   int32_t trace_cluster;
@@ -892,13 +894,14 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
   const int H = p.heads;
   const int ktiles = (p.n_kv + kPKeys - 1) / kPKeys;
   // clusters of a batch entry: the sink tiles' row splits first (they are as long as a full local tile and must
-  // not start late), then one per local tile
+  // not start late), then the local tiles, each in p.lsplit row splits (short sequences: fill the SMs)
   const int ns = p.sparse && p.nsplit > 1 ? (p.s < ktiles ? p.s : ktiles) : 0;
-  const int units = ns * p.nsplit + (ktiles - ns);
+  const int units = ns * p.nsplit + (ktiles - ns) * p.lsplit;
   const int pc = (int)(blockIdx.x >> 1);
   const int bi = pc / units, u = pc - bi * units;
-  const int tile = u < ns * p.nsplit ? u / p.nsplit : ns + (u - ns * p.nsplit);
-  const int ys = u < ns * p.nsplit ? u - tile * p.nsplit : 0;  // row split of a sink tile
+  const bool sink_unit = u < ns * p.nsplit;
+  const int tile = sink_unit ? u / p.nsplit : ns + (u - ns * p.nsplit) / p.lsplit;
+  const int ys = sink_unit ? u - tile * p.nsplit : (u - ns * p.nsplit) % p.lsplit;  // row split of the tile
   const int j0 = tile * kPKeys;
   // rows attending keys [j0, j0 + 128) (b == 128: the tile is one block)
   int p0 = p.causal ? j0 : 0, p1 = p.q_start + p.n_q;
@@ -909,9 +912,11 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
   }
   if (p0 < p.q_start) p0 = p.q_start;
   const bool split = p.sparse && kb < p.s && p.nsplit > 1;
-  if (split) {  // sink tile: rows split by whole query blocks, walked in the local tiles' rotation
+  const bool lsplit = p.sparse && kb >= p.s && p.lsplit > 1;  // a local tile's row split: partials too
+  if (split || lsplit) {  // rows split by whole query blocks, walked in the local tiles' rotation
     if (p1 > p0) {
-      const int ma = p0 / p.b, nb = (p1 - 1) / p.b - ma + 1, cb = (nb + p.nsplit - 1) / p.nsplit;
+      const int nsp = split ? p.nsplit : p.lsplit;
+      const int ma = p0 / p.b, nb = (p1 - 1) / p.b - ma + 1, cb = (nb + nsp - 1) / nsp;
       const int a = (ma + ys * cb) * p.b, e = a + cb * p.b;
       if (a > p0) p0 = a;
       if (e < p1) p1 = e;
@@ -1294,6 +1299,9 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
           if (split) {  // partials in the 32-key tile layout of the sink reduce: [B][n_sink][nsplit][32][1088]
             const int t32 = j >> 5, kl = j & 31;
             p.part[((((int64_t)bi * p.n_sink + t32) * p.nsplit + ys) * kKeys + kl) * kDkv + (kDvK ? kDqk : 0) + dim] = x;
+          } else if (lsplit) {  // [B][kt - ns][lsplit][128][1088]
+            p.part_local[((((int64_t)bi * (ktiles - ns) + (tile - ns)) * p.lsplit + ys) * kPKeys + (j - j0)) * kDkv +
+                         (kDvK ? kDqk : 0) + dim] = x;
           } else if (kDvK) {
             p.dv[((int64_t)bi * p.n_kv + j) * kDv + dim] = x;
           } else {
@@ -1315,6 +1323,33 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
     tc_fence_after();
     tmem_dealloc<2>(tmem, 512);
   }
+}
+
+// dK, dV of the local tiles that ran in row splits: the fixed-order sum of their partials
+__global__ void __launch_bounds__(256) bwd_local_reduce_kernel(const float* __restrict__ part, float* dk, float* dv,
+                                                               int32_t batch, int32_t n_kv, int32_t ns, int32_t nloc,
+                                                               int32_t lsplit) {
+  const int64_t per = (int64_t)nloc * kPKeys * (kDkv / 4);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)batch * per) return;
+  const int bi = (int)(i / per);
+  const int64_t rem = i - bi * per;
+  const int t = (int)(rem / (kPKeys * (kDkv / 4)));
+  const int r2 = (int)(rem - (int64_t)t * kPKeys * (kDkv / 4));
+  const int kl = r2 / (kDkv / 4), c = 4 * (r2 - kl * (kDkv / 4));
+  const int j = (ns + t) * kPKeys + kl;
+  if (j >= n_kv) return;
+  const float* src = part + ((((int64_t)bi * nloc + t) * lsplit) * kPKeys + kl) * kDkv + c;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int y = 0; y < lsplit; ++y) {
+    const float4 v = *reinterpret_cast<const float4*>(src + (int64_t)y * kPKeys * kDkv);
+    s.x += v.x;
+    s.y += v.y;
+    s.z += v.z;
+    s.w += v.w;
+  }
+  float* dst = c < kDqk ? dk + ((int64_t)bi * n_kv + j) * kDqk + c : dv + ((int64_t)bi * n_kv + j) * kDv + c - kDqk;
+  *reinterpret_cast<float4*>(dst) = s;
 }
 
 // ---------------------------------------------------------------------------------------------- dQ = dS K
@@ -1800,6 +1835,37 @@ cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk
 
 bool backward_pair_eligible(const AttnProblem& a) { return a.sparse && a.b == kPKeys; }
 
+// Row splits of the pair key kernels. A sink tile is attended by every row, a local tile by <= l query blocks;
+// both are cut into pieces of P whole query blocks, P the largest (up to l) whose clusters -- B x (sink tiles x
+// ceil(NB / P) + local tiles x ceil(l / P)) -- fit the device's cluster slots: at 8K one piece per local tile
+// (P = 7), at 2K P = 2. Split tiles write fp32 partials that a fixed-order reduce sums. Deterministic for a device.
+PairSplits backward_pair_splits(const AttnProblem& a) {
+  PairSplits r{1, 1};
+  if (!backward_pair_eligible(a) || a.n_kv == 0 || a.batch == 0 || a.n_q == 0) return r;
+  const int64_t kt = (a.n_kv + kPKeys - 1) / kPKeys;
+  const int64_t nb = ((int64_t)a.q_start + a.n_q + a.b - 1) / a.b - a.q_start / a.b;  // query blocks
+  const int64_t ns = a.s < kt ? a.s : kt;
+  const int64_t slots = device_sm_count() / 2;
+  int64_t P = a.l;
+  for (int64_t c = a.l; c >= 1; --c) {
+    const int64_t sn = a.s == 0 ? 1 : ((nb + c - 1) / c > 64 ? 64 : (nb + c - 1) / c);
+    const int64_t ls = (a.l + c - 1) / c;
+    if (a.batch * ((sn > 1 ? ns * sn : 0) + (kt - (sn > 1 ? ns : 0)) * ls) > slots) break;
+    P = c;
+  }
+  r.nsplit = a.s == 0 ? 1 : (int)((nb + P - 1) / P > 64 ? 64 : (nb + P - 1) / P);
+  r.lsplit = (int)((a.l + P - 1) / P);
+  return r;
+}
+int backward_local_splits(const AttnProblem& a) { return backward_pair_splits(a).lsplit; }
+size_t backward_local_part_bytes(const AttnProblem& a) {
+  const PairSplits sp = backward_pair_splits(a);
+  if (sp.lsplit <= 1) return 0;
+  const int64_t kt = (a.n_kv + kPKeys - 1) / kPKeys;
+  const int64_t ns = sp.nsplit > 1 ? (a.s < kt ? a.s : kt) : 0;
+  return sizeof(float) * (size_t)a.batch * (kt - ns) * sp.lsplit * kPKeys * kDkv;
+}
+
 // 64-key tiles (two kernels, dV then dK): the tile must lie in one block (b % 64 == 0) when sparse
 bool backward_key64_eligible(const AttnProblem& a) { return !a.sparse || a.b % k64Keys == 0; }
 
@@ -1808,8 +1874,8 @@ int g_bwd_trace_cluster = 0, g_bwd_trace_mode = 0;
 
 // 128-key CTA-pair kernels (dV, then dK reading P back from the dS row buffer): SSA with b == 128
 static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
-                                      float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st,
-                                      cudaEvent_t d_ready) {
+                                      float* part, float* part_local, uint16_t* ds, int nsplit, int n_sink,
+                                      cudaStream_t st, cudaEvent_t d_ready) {
   TcBwdParams p;
   const auto& kv = a.kv.seg[0];
   const uint64_t rows = (uint64_t)a.n_q * a.heads;
@@ -1858,7 +1924,11 @@ static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, fl
   if (!encode_4d_chunks(&pk.q1_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 1)) return cudaErrorInvalidValue;
   const int64_t kt = (a.n_kv + kPKeys - 1) / kPKeys;
   const int64_t ns = a.sparse && nsplit > 1 ? (a.s < kt ? a.s : kt) : 0;  // sink tiles, split over rows
-  const dim3 grid((unsigned)(2 * a.batch * (ns * nsplit + kt - ns)));
+  const int ls = backward_local_splits(a);
+  p.lsplit = pk.lsplit = ls;
+  p.part_local = pk.part_local = ls > 1 ? part_local : nullptr;
+  if (ls > 1 && !part_local) return cudaErrorInvalidValue;
+  const dim3 grid((unsigned)(2 * a.batch * (ns * nsplit + (kt - ns) * ls)));
   cudaError_t e = cudaFuncSetAttribute(bwd_pair_tc_kernel<kPairDv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<kPairDv>::kSmem);
   if (e == cudaSuccess)
@@ -1870,14 +1940,20 @@ static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, fl
   if (d_ready && (e = cudaStreamWaitEvent(st, d_ready, 0)) != cudaSuccess) return e;  // D (side stream) for dS
   bwd_pair_tc_kernel<kPairDk><<<grid, kPThreads, PairCfg<kPairDk>::kSmem, st>>>(pk);
   count_launch();
+  if (ls > 1) {
+    const int64_t n = (int64_t)a.batch * (kt - ns) * kPKeys * (kDkv / 4);
+    bwd_local_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part_local, dk, dv, a.batch, (int32_t)a.n_kv,
+                                                                         (int32_t)ns, (int32_t)(kt - ns), ls);
+    count_launch();
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
                                 float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st,
-                                cudaEvent_t d_ready, bool allow_pair) {
+                                cudaEvent_t d_ready, bool allow_pair, float* part_local) {
   if (allow_pair && ds && backward_pair_eligible(a))
-    return launch_bwd_pair_tc(a, dout, dk, dv, D, part, ds, nsplit, n_sink, st, d_ready);
+    return launch_bwd_pair_tc(a, dout, dk, dv, D, part, part_local, ds, nsplit, n_sink, st, d_ready);
   TcBwdParams p;
   const auto& kv = a.kv.seg[0];
   const uint64_t rows = (uint64_t)a.n_q * a.heads;

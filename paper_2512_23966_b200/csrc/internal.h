@@ -98,9 +98,16 @@ bool backward_ds_eligible(const AttnProblem& a);
 bool backward_key64_eligible(const AttnProblem& a);
 // d_ready (nullable): an event the dK kernel waits for (D computed on another stream, beside the dV kernel).
 // With the dS row buffer and b == 128 the 128-key CTA-pair kernels run instead unless allow_pair is false.
+// part_local: the pair kernels' local-tile row-split partials (backward_local_part_bytes), nullable when 0.
 cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
                                 float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st,
-                                cudaEvent_t d_ready = nullptr, bool allow_pair = true);
+                                cudaEvent_t d_ready = nullptr, bool allow_pair = true, float* part_local = nullptr);
+struct PairSplits {
+  int nsplit, lsplit;  // row splits of each sink tile / each local tile
+};
+PairSplits backward_pair_splits(const AttnProblem& a);
+int backward_local_splits(const AttnProblem& a);
+size_t backward_local_part_bytes(const AttnProblem& a);
 size_t backward_ds_bytes(const AttnProblem& a);
 cudaError_t launch_bwd_D(const AttnProblem& a, const void* dout, float* D, cudaStream_t st);
 // pair_keys: the key side ran the 128-key CTA-pair kernels (backward_pair_eligible), which write every slot of a
