@@ -96,16 +96,44 @@ def test_seqpar_validation():
     assert lib.loza_workspace_size(loza.LOZA_WS_SEQPAR, ctypes.byref(a2), loza.Pattern(1, 7, 128), 2) > 0
 
 
+def _bwd_ws_want(B, n, pat, H=64, slots=74):
+    """The backward workspace layout: D [B, n_q*H] fp32, the sink-tile partials
+    [B][ceil(s*b/32)][nsplit][32][1088] fp32, the local-tile row-split partials of the pair key kernels
+    [B][kt - ns][lsplit][128][1088] fp32 (each region 256-B aligned), then the dS rows [B, n_q*H, (s+l)*b] bf16.
+    Row splits: pieces of P whole query blocks, P the smallest <= l (scanning down from l) whose clusters
+    B x (sink tiles x ceil(NB/P) + local tiles x ceil(l/P)) fit the cluster slots (148 SMs / 2 without a GPU)."""
+    s, l, b = pat
+    al = lambda x: (x + 255) // 256 * 256  # noqa: E731
+    kt, nb = -(-n // 128), -(-n // b)
+    ns = min(s, kt)
+    P = l
+    for c in range(l, 0, -1):
+        sn = 1 if s == 0 else min(64, -(-nb // c))
+        if B * ((ns * sn if sn > 1 else 0) + (kt - (ns if sn > 1 else 0)) * -(-l // c)) > slots:
+            break
+        P = c
+    nsplit = 1 if s == 0 else min(64, -(-nb // P))
+    ls = -(-l // P)
+    sink = B * -(-min(s * b, n) // 32) * nsplit * 32 * 1088 * 4 if nsplit > 1 else 0
+    loc = B * (kt - (ns if nsplit > 1 else 0)) * ls * 128 * 1088 * 4 if ls > 1 else 0
+    return al(B * n * H * 4) + al(sink) + al(loc) + 2 * B * n * H * (s + l) * b
+
+
 @pytest.mark.parametrize("B,n,pat,want", [
-    # D [B, n_q*H] fp32 (256-B aligned), the sink-tile partials of the tensor-core key kernels
-    # (B x ceil(s*b/32) tiles x ceil(n_q/(l*b)) splits x 32 keys x 1088 fp32), then (SSA) the dS rows
-    # [B, n_q*H, (s+l)*b] bf16 the tcgen05 dQ GEMM reads (attn_bwd_mma.cu / attn_bwd_tc.cu)
+    # 8K: one piece per local tile (P = 7), 10 sink splits
     (2, 8192, (1, 7, 128), 2 * 8192 * 64 * 4 + 2 * 4 * 10 * 32 * 1088 * 4 + 2 * 2 * 8192 * 64 * 1024),
-    (1, 512, (1, 7, 128), 512 * 64 * 4 + 2 * 512 * 64 * 1024),                        # one split: no partials
+    # 512 tokens: P = 1, every tile split per query block (4 sink splits, 7 local splits)
+    (1, 512, (1, 7, 128), 512 * 64 * 4 + 4 * 4 * 32 * 1088 * 4 + 3 * 7 * 128 * 1088 * 4 + 2 * 512 * 64 * 1024),
     (1, 1024, (2, 1, 128), 1024 * 64 * 4 + 8 * 8 * 32 * 1088 * 4 + 2 * 1024 * 64 * 384),  # two sink blocks, 8 splits
-    (1, 1024, (0, 2, 128), 1024 * 64 * 4 + 2 * 1024 * 64 * 256),  # no sink blocks: no partials
+    (1, 1024, (0, 2, 128), 1024 * 64 * 4 + 8 * 2 * 128 * 1088 * 4 + 2 * 1024 * 64 * 256),  # no sink blocks, 2 local splits
+    (1, 4096, (1, 7, 128), None),  # P = 4
+    (3, 2048, (1, 7, 128), None),
 ])
 def test_backward_workspace_size(B, n, pat, want):
     """loza_workspace_size(LOZA_WS_BACKWARD) is what attention_backward checks against (host logic only)."""
     a = _args(batch=B, n_q=n, n_kv=n)
+    if want is None:
+        want = _bwd_ws_want(B, n, pat)
+    else:
+        assert _bwd_ws_want(B, n, pat) == want
     assert loza.lib().loza_workspace_size(loza.LOZA_WS_BACKWARD, ctypes.byref(a), loza.Pattern(*pat), 1) == want
