@@ -244,3 +244,38 @@ def test_backward_graph_capture_bitwise():
     torch.cuda.synchronize()
     for a, b in zip(out, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n,H,B,keys", [(2048, 8, 1, (5, 700, 1900)), (4096, 8, 1, (1300, 4000)),
+                                         (1024, 8, 3, (5, 900)), (4096, 64, 1, ())])
+def test_backward_pair_splits_repeat_bitwise(n, H, B, keys):
+    """The 128-key CTA-pair key kernels with their row splits (short sequences: every tile cut into query-block
+    pieces, partials summed by a fixed-order reduce) and the pair dQ GEMM: five calls give the
+    same bits (cross-CTA exchanges, DSMEM copies and partial reduces are ordered), and the dK / dV rows of
+    sampled keys -- a sink key, keys of early and late local blocks -- match the fp64 oracle backward over every
+    row that attends them (2e-2 normwise)."""
+    pat = (1, 7, 128)
+    qs = Spec(seed=71, tensor_id=TID_Q, batch=B, n=n, heads=H, d=576)
+    ks = Spec(seed=71, tensor_id=TID_K, batch=B, n=n, heads=1, d=576)
+    ds = Spec(seed=71, tensor_id=TID_DO, batch=B, n=n, heads=H, d=512)
+    q, kv, do = empty_filled(qs), empty_filled(ks), empty_filled(ds)
+    scale = loza.default_scale(576)
+    lse = torch.empty((B, H, n), device="cuda")
+    o = loza.ssa_prefill(q, kv, pattern=pat, scale=scale, lse=lse)
+    ref = loza.attention_backward(q, kv, o, lse, do, pattern=pat, scale=scale)
+    for _ in range(4):
+        out = loza.attention_backward(q, kv, o, lse, do, pattern=pat, scale=scale)
+        for a, b in zip(out, ref):
+            assert torch.equal(a, b)
+    _, dk, dv = ref
+    bi = B - 1
+    kf = gen_rows_f32(ks, bi * n, n)
+    for j in keys:  # rows attending key j: tokens j .. the end of its window (every token for a sink key)
+        t_hi = n if j < 128 else min(n, (j // 128 + 7) * 128)
+        toks = np.arange(j, t_hi)
+        _, rk, rv = oracle.attention_backward(gen_rows_f32(qs, (bi * n + j) * H, (t_hi - j) * H),
+                                              np.repeat(toks, H), kf, kf[:, :512],
+                                              gen_rows_f32(ds, (bi * n + j) * H, (t_hi - j) * H), scale,
+                                              *pat, sparse=True, causal=True)
+        assert _norm_err(dk[bi, j].double().cpu().numpy()[None], rk[j][None]) <= 2e-2
+        assert _norm_err(dv[bi, j].double().cpu().numpy()[None], rv[j][None]) <= 2e-2
