@@ -91,7 +91,7 @@ loza_status_t ssa_prefill(const loza_attn_args_t* args, loza_pattern_t pattern, 
  * the sink block(s) and the last l blocks of the cache, so its cost is
  * independent of the context length. args->n_q must be 1; args->n_kv = cache
  * capacity T_cap; seq_lens_dev [B] int32 on the device, 1 <= seq_len <= T_cap. q [B,1,H,d_qk] ->
- * o [B,1,H,d_v].
+ * o [B,1,H,d_v]. batch == 0 returns LOZA_OK without touching anything (seq_lens_dev may then be NULL).
  * ws: loza_workspace_size(LOZA_WS_DECODE, ...) bytes, initialised ONCE with loza_workspace_init (or any zero
  * fill) before its first use; every call leaves it reusable. Bytes [0, 4) are an int32 status word: the
  * kernels set it to LOZA_ERR_SHAPE when a seq_len was outside [1, T_cap] (they clamp it and continue); the
@@ -151,7 +151,8 @@ loza_status_t ssa_prefill_blend(const loza_attn_args_t* args, loza_pattern_t pat
  *   d_q [B, n_q, H, d_qk] = scale * sum_j dS_rj k_j,    dS_rj = P_rj (d_o_r . v_j - d_o_r . o_r)
  *   d_k [B, n_kv, d_qk]   = scale * sum_r dS_rj q_r,    P_rj  = exp(scale q_r . k_j - lse_r)
  *   d_v [B, n_kv, d_v]    = sum_r P_rj d_o_r
- * summed over every query row (all heads) that attends the key. For the absorbed MLA cache (v = the first
+ * summed over every query row (all heads) that attends the key (n_q == 0: d_k = d_v = 0, and d_o, lse, d_q
+ * may be NULL). For the absorbed MLA cache (v = the first
  * d_v columns of k) the cache gradient is d_k + [d_v, 0]. Deterministic (no atomics), fp32 accumulation;
  * d_qk <= 576, d_v <= 512 (else LOZA_ERR_UNSUPPORTED). bf16 with d_qk 576, d_v 512 and v aliasing k runs
  * on the tensor cores (tcgen05 when q / d_o rows are packed token x head; P and dS enter the second

@@ -158,6 +158,7 @@ loza_status_t ssa_prefill(const loza_attn_args_t* args, loza_pattern_t pattern, 
 loza_status_t ssa_decode(const loza_attn_args_t* args, const int32_t* seq_lens_dev, loza_pattern_t pattern,
                          void* ws, size_t ws_bytes, loza_stream_t stream) {
   g_last_error[0] = 0;
+  if (args && args->batch == 0) return LOZA_OK;  // nothing to decode (seq_lens may be NULL)
   if (!seq_lens_dev) return fail(LOZA_ERR_INVALID, "seq_lens_dev is NULL");
   AttnProblem p;
   loza_status_t rc = make_problem(args, true, pattern, seq_lens_dev, &p);
@@ -233,6 +234,14 @@ loza_status_t attention_backward(const loza_attn_args_t* args, int32_t sparse, l
   loza_pattern_t none = {0, 1, 1};
   loza_status_t rc = make_problem(args, sparse != 0, sparse ? pattern : none, nullptr, &p);
   if (rc != LOZA_OK) return rc;
+  if ((int64_t)p.batch * p.n_q == 0) {  // no query rows: every key gradient is zero (d_o, lse, d_q unused)
+    if ((int64_t)p.batch * p.n_kv == 0) return LOZA_OK;
+    if (!d_k || !d_v) return fail(LOZA_ERR_INVALID, "NULL gradient pointer");
+    cudaError_t e = cudaMemsetAsync(d_k, 0, sizeof(float) * (size_t)p.batch * p.n_kv * args->d_qk, (cudaStream_t)stream);
+    if (e == cudaSuccess)
+      e = cudaMemsetAsync(d_v, 0, sizeof(float) * (size_t)p.batch * p.n_kv * args->d_v, (cudaStream_t)stream);
+    return cuda_status(e, "backward (no query rows) memset");
+  }
   if (!args->lse) return fail(LOZA_ERR_INVALID, "attention_backward needs the forward's lse");
   if (!d_o || !d_q || !d_k || !d_v) return fail(LOZA_ERR_INVALID, "NULL gradient pointer");
   if (args->d_qk > 576 || args->d_v > 512) return fail(LOZA_ERR_UNSUPPORTED, "d_qk <= 576 and d_v <= 512");
@@ -294,6 +303,7 @@ loza_status_t ssa_ring_append(const void* rows, int64_t rows_stride_b, int64_t r
 loza_status_t ssa_decode_ring(const loza_attn_args_t* args, const int32_t* seq_lens_dev, loza_pattern_t pattern,
                               loza_stream_t stream) {
   g_last_error[0] = 0;
+  if (args && args->batch == 0) return LOZA_OK;  // nothing to decode (seq_lens may be NULL)
   if (!seq_lens_dev) return fail(LOZA_ERR_INVALID, "seq_lens_dev is NULL");
   AttnProblem p;
   loza_status_t rc = make_problem(args, true, pattern, seq_lens_dev, &p);

@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
   const int ktiles = (p.n_kv + kPKeys - 1) / kPKeys;
   // clusters of a batch entry: the sink tiles' row splits first (they are as long as a full local tile and must
   // not start late), then the local tiles, each in p.lsplit row splits (short sequences: fill the SMs)
-  const int ns = p.sparse && p.nsplit > 1 ? (p.s < ktiles ? p.s : ktiles) : 0;
+  const int ns = p.sparse ? (p.s < ktiles ? p.s : ktiles) : 0;  // sink tiles (nsplit units each, 1 if unsplit)
   const int units = ns * p.nsplit + (ktiles - ns) * p.lsplit;
   const int pc = (int)(blockIdx.x >> 1);
   const int bi = pc / units, u = pc - bi * units;
@@ -1850,7 +1850,7 @@ PairSplits backward_pair_splits(const AttnProblem& a) {
   for (int64_t c = a.l; c >= 1; --c) {
     const int64_t sn = a.s == 0 ? 1 : ((nb + c - 1) / c > 64 ? 64 : (nb + c - 1) / c);
     const int64_t ls = (a.l + c - 1) / c;
-    if (a.batch * ((sn > 1 ? ns * sn : 0) + (kt - (sn > 1 ? ns : 0)) * ls) > slots) break;
+    if (a.batch * (ns * sn + (kt - ns) * ls) > slots) break;
     P = c;
   }
   r.nsplit = a.s == 0 ? 1 : (int)((nb + P - 1) / P > 64 ? 64 : (nb + P - 1) / P);
@@ -1862,7 +1862,8 @@ size_t backward_local_part_bytes(const AttnProblem& a) {
   const PairSplits sp = backward_pair_splits(a);
   if (sp.lsplit <= 1) return 0;
   const int64_t kt = (a.n_kv + kPKeys - 1) / kPKeys;
-  const int64_t ns = sp.nsplit > 1 ? (a.s < kt ? a.s : kt) : 0;
+  const int64_t ns = a.s < kt ? a.s : kt;
+  if (kt - ns <= 0) return 0;
   return sizeof(float) * (size_t)a.batch * (kt - ns) * sp.lsplit * kPKeys * kDkv;
 }
 
@@ -1923,11 +1924,11 @@ static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, fl
   // the dK kernel's q1 box: [1 chunk][128 rows] (dK^T's third dim group)
   if (!encode_4d_chunks(&pk.q1_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 1)) return cudaErrorInvalidValue;
   const int64_t kt = (a.n_kv + kPKeys - 1) / kPKeys;
-  const int64_t ns = a.sparse && nsplit > 1 ? (a.s < kt ? a.s : kt) : 0;  // sink tiles, split over rows
+  const int64_t ns = a.s < kt ? a.s : kt;  // sink tiles (nsplit clusters each), then the local tiles (ls each)
   const int ls = backward_local_splits(a);
   p.lsplit = pk.lsplit = ls;
   p.part_local = pk.part_local = ls > 1 ? part_local : nullptr;
-  if (ls > 1 && !part_local) return cudaErrorInvalidValue;
+  if (ls > 1 && kt > ns && !part_local) return cudaErrorInvalidValue;
   const dim3 grid((unsigned)(2 * a.batch * (ns * nsplit + (kt - ns) * ls)));
   cudaError_t e = cudaFuncSetAttribute(bwd_pair_tc_kernel<kPairDv>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        PairCfg<kPairDv>::kSmem);
@@ -1940,7 +1941,7 @@ static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, fl
   if (d_ready && (e = cudaStreamWaitEvent(st, d_ready, 0)) != cudaSuccess) return e;  // D (side stream) for dS
   bwd_pair_tc_kernel<kPairDk><<<grid, kPThreads, PairCfg<kPairDk>::kSmem, st>>>(pk);
   count_launch();
-  if (ls > 1) {
+  if (ls > 1 && kt > ns) {
     const int64_t n = (int64_t)a.batch * (kt - ns) * kPKeys * (kDkv / 4);
     bwd_local_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part_local, dk, dv, a.batch, (int32_t)a.n_kv,
                                                                          (int32_t)ns, (int32_t)(kt - ns), ls);

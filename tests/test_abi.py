@@ -109,13 +109,13 @@ def _bwd_ws_want(B, n, pat, H=64, slots=74):
     P = l
     for c in range(l, 0, -1):
         sn = 1 if s == 0 else min(64, -(-nb // c))
-        if B * ((ns * sn if sn > 1 else 0) + (kt - (ns if sn > 1 else 0)) * -(-l // c)) > slots:
+        if B * (ns * sn + (kt - ns) * -(-l // c)) > slots:
             break
         P = c
     nsplit = 1 if s == 0 else min(64, -(-nb // P))
     ls = -(-l // P)
     sink = B * -(-min(s * b, n) // 32) * nsplit * 32 * 1088 * 4 if nsplit > 1 else 0
-    loc = B * (kt - (ns if nsplit > 1 else 0)) * ls * 128 * 1088 * 4 if ls > 1 else 0
+    loc = B * (kt - ns) * ls * 128 * 1088 * 4 if ls > 1 else 0
     return al(B * n * H * 4) + al(sink) + al(loc) + 2 * B * n * H * (s + l) * b
 
 
@@ -128,6 +128,8 @@ def _bwd_ws_want(B, n, pat, H=64, slots=74):
     (1, 1024, (0, 2, 128), 1024 * 64 * 4 + 8 * 2 * 128 * 1088 * 4 + 2 * 1024 * 64 * 256),  # no sink blocks, 2 local splits
     (1, 4096, (1, 7, 128), None),  # P = 4
     (3, 2048, (1, 7, 128), None),
+    (1, 128, (1, 7, 128), None),  # one block, the sink: no local tiles, no partials
+    (1, 256, (2, 7, 128), None),
 ])
 def test_backward_workspace_size(B, n, pat, want):
     """loza_workspace_size(LOZA_WS_BACKWARD) is what attention_backward checks against (host logic only)."""
