@@ -100,3 +100,37 @@ def test_ragged_tiny_prefill_vs_oracle():
                                    loza.default_scale(DQK), 1, 1, 128, sparse=True, causal=True)
     got = o[0].reshape(n * H, DV).double().cpu().numpy()
     assert np.abs(got - ref).max() <= 2e-2
+
+
+@pytest.mark.parametrize("n,Hh,pat", [(130, 64, (1, 7, 128)), (257, 8, (1, 7, 128)), (200, 1, (1, 2, 128)),
+                                      (384, 16, (2, 3, 128)), (129, 64, (0, 3, 128)), (1, 64, (1, 7, 128))])
+def test_backward_small_shapes_vs_oracle(n, Hh, pat):
+    """Short and ragged SSA backward problems (a partial last block, one head, no sink blocks, two sink blocks,
+    a single token) through the default path (CTA-pair key kernels with row splits, dQ GEMM): every dQ row and
+    every dK / dV row against the fp64 oracle backward (2e-2 normwise)."""
+    qs = Spec(seed=93, tensor_id=TID_Q, batch=1, n=n, heads=Hh, d=DQK)
+    ks = Spec(seed=93, tensor_id=TID_K, batch=1, n=n, heads=1, d=DQK)
+    dos = Spec(seed=93, tensor_id=TID_DO, batch=1, n=n, heads=Hh, d=DV)
+    q, kv, do = empty_filled(qs), empty_filled(ks), empty_filled(dos)
+    scale = loza.default_scale(DQK)
+    kf = gen_rows_f32(ks, 0, n)
+    # O and LSE from the oracle forward (the bf16 prefill takes n_q * H % 128 == 0 or H % 64 == 0 only)
+    orow, lrow = oracle.attention_rows(gen_rows_f32(qs, 0, n * Hh), np.repeat(np.arange(n), Hh), kf, kf[:, :DV],
+                                       scale, *pat, sparse=True, causal=True)
+    o = torch.from_numpy(orow.reshape(1, n, Hh, DV)).to(torch.bfloat16).cuda()
+    lse = torch.from_numpy(lrow.reshape(n, Hh).T.copy()[None]).float().cuda()
+    dq, dk, dv = loza.attention_backward(q, kv, o, lse, do, pattern=pat, scale=scale)
+    torch.cuda.synchronize()
+    rq, rk, rv = oracle.attention_backward(gen_rows_f32(qs, 0, n * Hh), np.repeat(np.arange(n), Hh), kf, kf[:, :DV],
+                                           gen_rows_f32(dos, 0, n * Hh), scale, *pat, sparse=True, causal=True)
+
+    # normwise, floored at 1e-3 of the dV norm: with one key (n = 1) dq and dk are exactly 0 in the oracle and
+    # bf16 rounding of o leaves ~1e-8 (dS = P (dO.v - dO.o))
+    floor = 1e-3 * np.linalg.norm(rv)
+
+    def err(got, ref):
+        return np.linalg.norm(got - ref) / max(np.linalg.norm(ref), floor)
+
+    assert err(dq[0].reshape(-1, DQK).double().cpu().numpy(), rq) <= 2e-2
+    assert err(dk[0].double().cpu().numpy(), rk) <= 2e-2
+    assert err(dv[0].double().cpu().numpy(), rv) <= 2e-2
