@@ -37,7 +37,7 @@ def _oracle(qs, ks, bi, L, pattern, H):
     return oracle.attend(qr, kf, kf[:, :D_V], SCALE)
 
 
-@pytest.mark.parametrize("H", [8, 16, 32, 48])
+@pytest.mark.parametrize("H", [1, 8, 16, 32, 48, 63])
 @pytest.mark.parametrize("pattern", [(1, 7, 128), (2, 3, 256), (0, 3, 128)])
 @pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
 def test_decode_head_sharded_vs_oracle(H, pattern, out_dtype):
