@@ -188,3 +188,16 @@ def test_chunked_prefill_bitwise():
         loza.ssa_prefill(q[:, a:a + nc], kv[:, :a + nc], pattern=pat, scale=SCALE, out=out[:, a:a + nc], q_start=a)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("n,H,pat", [(1024, 8, (1, 7, 128)), (256, 128, (1, 1, 128)), (640, 2, (1, 2, 128)),
+                                     (200, 16, (1, 7, 128)), (384, 192, (2, 1, 128))])
+def test_ssa_prefill_head_counts(n, H, pat):
+    """The tcgen05 prefill at other head counts (a 128-row unit then spans 128 / H tokens, or a token spans several
+    units): H = 2, 8, 16 (n_q * H % 128 == 0), 128 and 192 (H % 64 == 0); every token against the oracle."""
+    qs, ks = _specs(21 + H, 1, n, H)
+    q, kv = empty_filled(qs), empty_filled(ks)
+    lse = torch.empty((1, H, n), device="cuda")
+    o = loza.ssa_prefill(q, kv, pattern=pat, scale=SCALE, lse=lse, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    _check_rows(o, lse, qs, ks, range(n), pat, True)
