@@ -15,6 +15,7 @@
 // (one 4-D TMA box, 32 KB) through a 5-slot ring, twice per row tile (S/dP, then dK^T/dV^T): the tile does
 // not fit shared memory whole. Warp roles: 0 TMA, 1 UMMA issue (+ TMEM alloc), 4-7 P/dS and the epilogue.
 #include <math.h>
+#include <string.h>
 
 #include "internal.h"
 #include "sm100.cuh"
@@ -1791,6 +1792,7 @@ bool backward_tc_eligible(const AttnProblem& a, const void* dout) {
 cudaError_t launch_bwd_dkdv_tc(const AttnProblem& a, const void* dout, float* dk, float* dv, const float* D,
                                float* part, uint16_t* ds, int nsplit, int n_sink, cudaStream_t st) {
   TcBwdParams p;
+  memset(&p, 0, sizeof(p));  // debug / pair-only fields default to off
   const auto& kv = a.kv.seg[0];
   const uint64_t rows = (uint64_t)a.n_q * a.heads;
   if (!encode_4d_chunks(&p.q_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 2) ||
@@ -1878,6 +1880,7 @@ static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, fl
                                       float* part, float* part_local, uint16_t* ds, int nsplit, int n_sink,
                                       cudaStream_t st, cudaEvent_t d_ready) {
   TcBwdParams p;
+  memset(&p, 0, sizeof(p));  // debug / pair-only fields default to off
   const auto& kv = a.kv.seg[0];
   const uint64_t rows = (uint64_t)a.n_q * a.heads;
   TcBwdParams pk;  // the dK kernel's: its K tile is V's 8 chunks
@@ -1956,6 +1959,7 @@ cudaError_t launch_bwd_key64_tc(const AttnProblem& a, const void* dout, float* d
   if (allow_pair && ds && backward_pair_eligible(a))
     return launch_bwd_pair_tc(a, dout, dk, dv, D, part, part_local, ds, nsplit, n_sink, st, d_ready);
   TcBwdParams p;
+  memset(&p, 0, sizeof(p));  // debug / pair-only fields default to off
   const auto& kv = a.kv.seg[0];
   const uint64_t rows = (uint64_t)a.n_q * a.heads;
   if (!encode_4d_chunks(&p.q_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 2) ||
@@ -2035,6 +2039,7 @@ cudaError_t launch_bwd_D(const AttnProblem& a, const void* dout, float* D, cudaS
 
 cudaError_t launch_bwd_dq_tc(const AttnProblem& a, const uint16_t* ds, float* dq, cudaStream_t st, bool pair_keys) {
   TcDqParams p;
+  memset(&p, 0, sizeof(p));
   const auto& kv = a.kv.seg[0];
   const int W = (a.s + a.l) * a.b;
   const uint64_t rows = (uint64_t)a.n_q * a.heads;
