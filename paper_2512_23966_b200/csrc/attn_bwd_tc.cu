@@ -846,6 +846,9 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
 // dK^T 3 x 128 + dP 2 x 64. SMEM: ring 3 x 32 KB, K tile 72 KB (dV: 9 chunks) or 64 KB (dK: V's 8), P / dS
 // 2 x 16 KB, staging 2 x 8 KB. Warps 0-7 P / dS and the epilogue (warp w: TMEM lane quarter w % 4, column half w / 4),
 // warp 8 TMA, warp 9 UMMA issue (leader) and TMEM allocation, warp 10 the DSMEM copy.
+#ifndef BWD_DK_G2_M128
+#define BWD_DK_G2_M128 1
+#endif
 constexpr int kPairDv = 1, kPairDk = 2;
 constexpr int kPKeys = 128, kPHalf = 64;  // keys per pair tile; rows of a 128-row tile per CTA
 constexpr int kPThreads = 352, kPProd = 8, kPMma = 9, kPXfer = 10;
@@ -861,7 +864,9 @@ struct PairCfg {
   // and the DSMEM copy of tile tc overlap the P of tile tc + 1
   static constexpr int kOffRing = 0, kOffK = kStages * kPairBytes, kOffP = kOffK + kKBytes,
                        kOffSt = kOffP + 2 * kPBytes, kOffBar = kOffSt + 2 * kStBytes;
-  static constexpr int kSBufs = kDv ? 4 : 2, kAhead = kSBufs - 1;  // S / dP buffers, first-pass lookahead
+  // S / dP buffers and the first-pass lookahead (dK: dK^T's third dim group as an M128 UMMA takes 64 columns,
+  // which leaves room for a third dP buffer)
+  static constexpr int kSBufs = kDv ? 4 : (BWD_DK_G2_M128 ? 3 : 2), kAhead = kSBufs - 1;
   static constexpr int kBarFull = 0, kBarEmpty = kStages, kBarK = 2 * kStages, kBarSFull = kBarK + 1,
                        kBarSFree = kBarSFull + kSBufs, kBarPLocal = kBarSFree + kSBufs, kBarPStaged = kBarPLocal + 2,
                        kBarPRecv = kBarPStaged + 2, kBarPFull = kBarPRecv + 2, kBarPFree = kBarPFull + 2,
@@ -870,7 +875,7 @@ struct PairCfg {
   static constexpr int kSmem = kOffTmemPtr + 16 + 1024;
   static constexpr int kFirstItems = kDv ? 3 : 2;  // Q (chunks 0-3, 4-7, 8) or dO (0-3, 4-7) of this CTA's 64 rows
   static constexpr int kGroups = kDv ? 2 : 3;      // 256-dim M groups of dV^T / dK^T
-  static constexpr uint32_t kTmemS = kDv ? 0 : 384, kTmemAcc = kDv ? 256 : 0;
+  static constexpr uint32_t kTmemS = kDv ? 0 : (BWD_DK_G2_M128 ? 320 : 384), kTmemAcc = kDv ? 256 : 0;
 };
 static_assert(PairCfg<kPairDv>::kSmem <= 232448 && PairCfg<kPairDk>::kSmem <= 232448, "smem");
 
@@ -1098,12 +1103,15 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
         tc_fence_after();
         const uint32_t pb = sbase + C::kOffP + (tc & 1) * C::kPBytes;
         for (int g = 0; g < C::kGroups; ++g) {
+          // dK^T dims 512..575 (CTA 0's one chunk): an M128 UMMA, 64 rows per CTA, D folded over the lanes
+          const bool m128 = !kDvK && BWD_DK_G2_M128 && g == 2;
+          constexpr uint32_t id_t2 = idesc_bf16_f32(128, kPKeys, true, true);
           take();
           if (elect_one()) {
             for (int kr = 0; kr < 8; ++kr)
               umma_bf16_pair(tmem + C::kTmemAcc + 128 * g,
                              sdesc_sw128(sbase + C::kOffRing + slot * kPairBytes + 2048 * kr, 16384, 1024),
-                             sdesc_sw128(pb + 2048 * kr, 16, 1024), id_t, (tc | kr) != 0);
+                             sdesc_sw128(pb + 2048 * kr, 16, 1024), m128 ? id_t2 : id_t, (tc | kr) != 0);
           }
           release();
         }
@@ -1279,14 +1287,18 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       tc_fence_after();
     }
     for (int g = 0; g < C::kGroups; ++g) {
-      const int d0 = 256 * g + 128 * (int)rank + 32 * q, dim = d0 + lane;
+      const bool m128 = !kDvK && BWD_DK_G2_M128 && g == 2;
+      // M256 groups: lane = dim 256 g + 128 rank + lane, column = key. The M128 group (dims 512..575, CTA 0):
+      // lanes 0-63 hold the dims for keys 0-63, lanes 64-127 the same dims for keys 64-127
+      const int d0 = m128 ? (rank == 0 ? 512 + 32 * (q & 1) : kDqk) : 256 * g + 128 * (int)rank + 32 * q;
+      const int dim = d0 + lane;
       if (d0 >= (kDvK ? kDv : kDqk)) continue;  // warp-uniform: the zero-filled dims of dK^T's third group
       const float sc = kDvK ? 1.f : p.scale;
 #pragma unroll 1
-      for (int hf = 0; hf < 2; ++hf) {
+      for (int hf = 0; hf < (m128 ? 1 : 2); ++hf) {
         uint32_t v[32];
         if (any) {
-          tmem_ld32(tl + C::kTmemAcc + 128 * g + 64 * c + 32 * hf, v);
+          tmem_ld32(tl + C::kTmemAcc + 128 * g + (m128 ? 32 * c : 64 * c + 32 * hf), v);
           tmem_wait_ld();
         } else {
 #pragma unroll
@@ -1294,7 +1306,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
         }
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const int j = j0 + 64 * c + 32 * hf + e;
+          const int j = j0 + (m128 ? 64 * (q >> 1) + 32 * c : 64 * c + 32 * hf) + e;
           if (j >= p.n_kv) continue;
           const float x = __uint_as_float(v[e]) * sc;
           if (split) {  // partials in the 32-key tile layout of the sink reduce: [B][n_sink][nsplit][32][1088]
