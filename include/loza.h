@@ -158,7 +158,9 @@ loza_status_t ssa_prefill_blend(const loza_attn_args_t* args, loza_pattern_t pat
  * on the tensor cores (tcgen05 when q / d_o rows are packed token x head; P and dS enter the second
  * products as bf16), everything else on FFMA.
  * ws: loza_workspace_size(LOZA_WS_BACKWARD, args, pattern, 1) bytes: D [B, n_q*H] fp32, for SSA the sink-tile
- * partials and the dS rows [B, n_q*H, (s+l)*b] bf16 (1 GiB at B1, 8K tokens, H64, (1,7,128)). */
+ * partials, the local-tile row-split partials (short sequences, sized from the current device's SM count:
+ * query the size on the device that runs the call) and the dS rows [B, n_q*H, (s+l)*b] bf16 (1 GiB at B1, 8K
+ * tokens, H64, (1,7,128)). */
 loza_status_t attention_backward(const loza_attn_args_t* args, int32_t sparse, loza_pattern_t pattern,
                                  const void* d_o, float* d_q, float* d_k, float* d_v, void* ws, size_t ws_bytes,
                                  loza_stream_t stream);
