@@ -488,6 +488,7 @@ def extra_rows(args, q, kv, o, flush, peaks):
         "fused_ms": fu_ms, "unfused_ms": float(np.mean(t_ssa)) + float(np.mean(t_bl)),
         "speedup_vs_unfused": (float(np.mean(t_ssa)) + float(np.mean(t_bl))) / fu_ms,
         "fused_fwd_only_ms": float(np.mean(t_ff)), "unfused_fwd_only_ms": float(np.mean(t_ssa)) + float(np.mean(t_bf)),
+        "speedup_fwd_only_vs_unfused": (float(np.mean(t_ssa)) + float(np.mean(t_bf))) / float(np.mean(t_ff)),
         "ssa_frac_tensor_in_fused": ssa_pairs(n8, *PATTERN) * FLOP_PER_PAIR / (fu_ms * 1e-3) / 1e12
         / peaks["bf16_tflops"],
         "note": "unfused = ssa_prefill (writes O') + loza_blend with d_alpha (reads O, O', dO_hat; writes O_hat)"}

@@ -88,8 +88,13 @@ constexpr int kBarPFull = kBarSFree + 2;         // [1]
 constexpr int kBarOFull = kBarPFull + 1;         // [2]
 constexpr int kBarOFree = kBarOFull + 2;
 constexpr int kBarOfFull = kBarOFree + 1;   // calibration: O_full of the unit staged in the Q region (local)
-constexpr int kBarOfEmpty = kBarOfFull + 1;  // calibration: the epilogue has read it (8 softmax warps, local)
-constexpr int kNumBars = kBarOfEmpty + 1;
+// calibration: the epilogue has read the O_full box in Q chunk slot c ([8]; the 2 warps that read it, local)
+constexpr int kBarOfEmpty = kBarOfFull + 1;
+constexpr int kNumBars = kBarOfEmpty + 8;
+// O_full box m (dims 64 m ..) lives in Q chunk slot of_slot(m): the boxes the epilogue finishes first (its
+// warps' first 64 dims, m even) take slots 0-3, so the next unit's Q chunks 0-3 -- and the S UMMAs on them --
+// can start while the epilogue still works on the other half
+__host__ __device__ constexpr int of_slot(int m) { return (m & 1) * 4 + (m >> 1); }
 constexpr int kOffTmemPtr = kOffBar + kNumBars * 8;
 constexpr int kOffPub = kOffTmemPtr + 4;                // uint32 [2]: producers' next ring positions
 constexpr int kOffRed = (kOffPub + 8 + 15) & ~15;  // float [2 buf][4 quarter-rows][64]; epilogue reuses it
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     mbar_init(bar(kBarPFull), kArrivalsPerPair);
     mbar_init(bar(kBarOFree), kArrivalsPerPair);
     mbar_init(bar(kBarOfFull), 1);
-    mbar_init(bar(kBarOfEmpty), kSoftmaxWarps);
+    for (int i = 0; i < 8; ++i) mbar_init(bar(kBarOfEmpty + i), 2);
     reinterpret_cast<volatile uint32_t*>(smem + kOffPub)[0] = 0;
     reinterpret_cast<volatile uint32_t*>(smem + kOffPub)[1] = 0;
     fence_mbar_init();
@@ -317,7 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     RingPos rp;
     uint32_t uc = 0;
     uint32_t gk = 0;
-    auto load_k = [&](const Unit& U, int i) {
+    auto no_hook = [](int) {};
+    auto load_k = [&](const Unit& U, int i, auto&& before_item) {
       int sg;
       int32_t row;
       kv_coord(p, sub_k0(U, 2 * i + (int)rank), 0, sg, row);  // CTA r stages sub-block 2i+r
@@ -329,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       }
       __syncwarp();
       for (int j = 0; j < kKItems; ++j, rp.step()) {
+        before_item(j);
         acquire(rp, 0);
         if (j == 0) TRACE(13, gk);
         if (j == kKItems - 1) TRACE(14, gk);
@@ -348,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       if (elect_one()) {
         mbar_arrive_expect_tx(bar(kBarOfFull), 8 * 8192);
         for (int m = 0; m < 8; ++m)
-          tma_load_3d(sbase + kOffQ + m * 8192, &p.of_map, 64 * m, (int32_t)(Us.row0 + 64 * rank), Us.bi,
+          tma_load_3d(sbase + kOffQ + of_slot(m) * 8192, &p.of_map, 64 * m, (int32_t)(Us.row0 + 64 * rank), Us.bi,
                       bar(kBarOfFull), pol_q);
       }
       __syncwarp();
@@ -361,10 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       if (lane == 0) pub[0] = rp.pos;
       __syncwarp();
       if constexpr (kCalib) {
-        if (uc > 0) {
-          stage_o_full(Uprev, uc - 1);
-          mbar_wait(bar(kBarOfEmpty), (uc - 1) & 1);  // the previous unit's epilogue has read it
-        }
+        if (uc > 0) stage_o_full(Uprev, uc - 1);
         // d_o_hat rows of this unit into L2 ahead of the epilogue (read with plain loads there)
         if (p.d_o_hat) {
           const int64_t r0 = U.row0 + 64 * rank, rows_b = (int64_t)p.n_q * p.heads;
@@ -374,19 +378,35 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
             asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.d_o_hat + off + ln * 128));
         }
       }
-      for (int c = 0; c < kChunks; ++c) {
+      auto load_q = [&](int c) {
         mbar_wait(bar(kBarQEmpty + c), (uc & 1) ^ 1);
+        if (kCalib && uc > 0 && c < 8) {  // the previous unit's epilogue has read the O_full box in this slot
+          if (lane == 0) pub[0] = rp.pos;
+          __syncwarp();
+          mbar_wait(bar(kBarOfEmpty + c), (uc - 1) & 1);
+        }
         if (elect_one()) {
           if (rank == 0) mbar_arrive_expect_tx(bar(kBarQFull + c), 2 * 8192);
           tma_load_3d_pair(sbase + kOffQ + c * 8192, &p.q_map, c * 64, (int32_t)(U.row0 + 64 * rank), U.bi,
                            QFULL_L(c), pol_q);
         }
         __syncwarp();
+      };
+      if constexpr (kCalib) {
+        // Q chunk 8 (no O_full there), then each chunk pair as its slots are released, interleaved with the
+        // first tile's K items so the S UMMAs on chunks 0-3 overlap the previous unit's epilogue
+        load_q(8);
+        load_k(U, 0, [&](int j) {
+          load_q(2 * j);
+          load_q(2 * j + 1);
+        });
+        Uprev = U;
+      } else {
+        for (int c = 0; c < kChunks; ++c) load_q(c);
+        load_k(U, 0, no_hook);
       }
-      if constexpr (kCalib) Uprev = U;
-      load_k(U, 0);
       for (int i = 1; i < U.n_tiles; ++i) {
-        load_k(U, i);
+        load_k(U, i, no_hook);
         rp.skip(kVItems);  // V(i-1): warp kVWarp
       }
       rp.skip(kVItems);
@@ -762,11 +782,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
                 dn[q] = dload ? ldg_nc_v4(dhb + 64 * (c + 1) + 16 * q) : make_uint4(0, 0, 0, 0);
             }
             // O_full box m = dims [64 m, +64): row r at m * 8192 + 128 r, 16-B units swizzled by r & 7
-            const uint8_t* ofs = smem + kOffQ + (4 * ch + 2 * kh + (c >> 1)) * 8192 + r * 128;
+            const uint8_t* ofs = smem + kOffQ + of_slot(4 * ch + 2 * kh + (c >> 1)) * 8192 + r * 128;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const uint4 x4 = *reinterpret_cast<const uint4*>(ofs + ((((c & 1) * 4 + q) ^ (r & 7)) << 4));
               xw[4 * q] = x4.x; xw[4 * q + 1] = x4.y; xw[4 * q + 2] = x4.z; xw[4 * q + 3] = x4.w;
+            }
+            if (c & 1) {  // this warp is done with O_full box 4 ch + 2 kh + (c >> 1): its slot may take Q
+              __syncwarp();
+              if (lane == 0) mbar_arrive_local(bar(kBarOfEmpty + of_slot(4 * ch + 2 * kh + (c >> 1))));
             }
             tmem_wait_ld();
             uint32_t wc[16];
@@ -780,8 +804,6 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) w[16 * c + j] = wc[j];
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive_local(bar(kBarOfEmpty));  // the staged O_full may be replaced by Q
           gacc += (double)gs;
         }
         tc_fence_before();
