@@ -48,9 +48,16 @@ using namespace sm100;
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+#ifndef DOHAT_L1
+#define DOHAT_L1 1  // d_o_hat loads allocate in L1 (a thread's 4 x 16 B of one 64-B run share 2 sectors)
+#endif
 __device__ __forceinline__ uint4 ldg_nc_v4(const void* ptr) {
   uint4 r;
+#if DOHAT_L1
+  asm volatile("ld.global.nc.L1::evict_first.v4.u32 {%0,%1,%2,%3}, [%4];"
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+#endif
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(ptr));
   return r;
@@ -726,6 +733,17 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       }
       // ---------------- epilogue: O / l -> global (this warp: O columns [128 ch, +128) = dims 256 ch + 128 kh ..)
       const uint32_t gl = g + U.n_tiles - 1;
+      // calibration with d_o_hat: this row's first d_o_hat chunk is requested before the wait for the last PV
+      const int64_t doff = ((int64_t)U.bi * p.o_sb + row_g * kDv + 256 * (int)ch + 128 * (int)kh) * 2;
+      const uint8_t* dhb = calib && p.d_o_hat ? p.d_o_hat + doff : nullptr;
+      const bool dload = calib && row_ok && dhb;
+      uint4 dn[4], dn2[4];
+      if constexpr (calib) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dn[q] = dload ? ldg_nc_v4(dhb + 16 * q) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dn2[q] = dload ? ldg_nc_v4(dhb + 64 + 16 * q) : make_uint4(0, 0, 0, 0);
+      }
       mbar_wait(bar(kBarOFull + (gl & 1)), (gl >> 1) & 1);
       tc_fence_after();
       float* ls = red + ((gl + 1) & 1) * 256;  // the exchange buffer not used by the last tile
@@ -757,16 +775,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           // Eq. 3 on this thread's 128 outputs: o_hat = fma(alpha, O, (1 - alpha) O') with O' the fp32 SSA
           // result (alpha = 0 gives exactly the plain bf16 output, alpha = 1 gives O), and
           // d_alpha += d_o_hat (O - O'). O and d_o_hat are read straight from global (bf16, 64 B per chunk).
-          const int64_t off = ((int64_t)U.bi * p.o_sb + row_g * kDv + 256 * (int)ch + 128 * (int)kh) * 2;
-          const uint8_t* dhb = p.d_o_hat ? p.d_o_hat + off : nullptr;
           float gs = 0.f;
           mbar_wait(bar(kBarOfFull), uc & 1);  // this unit's O_full rows, staged in the Q region
-          // d_o_hat chunks are software-pipelined one chunk ahead: the loads of chunk c + 1 are in flight
-          // while chunk c is converted (the TMEM wait's memory clobber would otherwise serialise 4 L2 latencies)
-          const bool dload = row_ok && dhb;
-          uint4 dn[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) dn[q] = dload ? ldg_nc_v4(dhb + 16 * q) : make_uint4(0, 0, 0, 0);
+          // d_o_hat chunks are software-pipelined one chunk ahead (chunk 0 was requested before the last PV's
+          // wait): the loads of chunk c + 1 are in flight while chunk c is converted (the TMEM wait's memory
+          // clobber would otherwise serialise 4 L2 latencies)
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t ov[32];
@@ -776,10 +789,10 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
             for (int q = 0; q < 4; ++q) {
               dw[4 * q] = dn[q].x; dw[4 * q + 1] = dn[q].y; dw[4 * q + 2] = dn[q].z; dw[4 * q + 3] = dn[q].w;
             }
-            if (c < 3) {
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                dn[q] = dload ? ldg_nc_v4(dhb + 64 * (c + 1) + 16 * q) : make_uint4(0, 0, 0, 0);
+            for (int q = 0; q < 4; ++q) {  // two chunks ahead
+              dn[q] = dn2[q];
+              if (c < 2) dn2[q] = dload ? ldg_nc_v4(dhb + 64 * (c + 2) + 16 * q) : make_uint4(0, 0, 0, 0);
             }
             // O_full box m = dims [64 m, +64): row r at m * 8192 + 128 r, 16-B units swizzled by r & 7
             const uint8_t* ofs = smem + kOffQ + of_slot(4 * ch + 2 * kh + (c >> 1)) * 8192 + r * 128;
