@@ -376,13 +376,15 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       __syncwarp();
       if constexpr (kCalib) {
         if (uc > 0) stage_o_full(Uprev, uc - 1);
-        // d_o_hat rows of this unit into L2 ahead of the epilogue (read with plain loads there)
-        if (p.d_o_hat) {
+        // d_o_hat rows of this unit into L2 ahead of the epilogue (read with plain loads there; an L2
+        // prefetch of the O_full rows as well measured slower)
+        {
           const int64_t r0 = U.row0 + 64 * rank, rows_b = (int64_t)p.n_q * p.heads;
           const int64_t nl = ((rows_b - r0 < 64 ? rows_b - r0 : 64) * kDv * 2) / 128;
           const int64_t off = ((int64_t)U.bi * p.o_sb + r0 * kDv) * 2;
-          for (int64_t ln = lane; ln < nl; ln += 32)
-            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.d_o_hat + off + ln * 128));
+          for (int64_t ln = lane; ln < nl; ln += 32) {
+            if (p.d_o_hat) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.d_o_hat + off + ln * 128));
+          }
         }
       }
       auto load_q = [&](int c) {
