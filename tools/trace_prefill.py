@@ -15,11 +15,29 @@ o = torch.empty((1, n, H, 512), dtype=torch.bfloat16, device="cuda")
 tr = torch.zeros(22 * 64, dtype=torch.int64, device="cuda")
 L = loza.lib()
 L.loza_debug_set_trace.argtypes = [ctypes.c_void_p]
+if mode in ("calib", "calibf"):  # fused calibration with d_o_hat (ssa_prefill_blend), or forward only
+    of = torch.empty_like(o)
+    loza.full_attn_ref(q, kv, out=of)
+    dh = empty_filled(Spec(seed=0, tensor_id=TID_Q, batch=1, n=n, heads=H, d=512))
+    alpha = torch.tensor([0.5], device="cuda")
+
+
+def run():
+    if mode == "ssa":
+        loza.ssa_prefill(q, kv, out=o)
+    elif mode == "calib":
+        loza.ssa_prefill_blend(q, kv, of, alpha, dh, out=o)
+    elif mode == "calibf":
+        loza.ssa_prefill_blend(q, kv, of, alpha, out=o)
+    else:
+        loza.full_attn_ref(q, kv, out=o)
+
+
 for _ in range(2):
-    (loza.ssa_prefill(q, kv, out=o) if mode == "ssa" else loza.full_attn_ref(q, kv, out=o))
+    run()
 torch.cuda.synchronize()
 L.loza_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
-(loza.ssa_prefill(q, kv, out=o) if mode == "ssa" else loza.full_attn_ref(q, kv, out=o))
+run()
 torch.cuda.synchronize()
 L.loza_debug_set_trace(ctypes.c_void_p(0))
 t = tr.view(22, 64).cpu().numpy().astype("int64")
