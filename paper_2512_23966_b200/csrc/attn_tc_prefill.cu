@@ -230,11 +230,12 @@ __device__ __forceinline__ int64_t unit_index(const PrefillParams& p, int64_t it
     if (p.trace && cid == 0 && rank == 0 && (idx) < 64 && lane == 0) p.trace[(slot)*64 + (idx)] = clock64(); \
   } while (0)
 
-// kCalib: fused calibration forward (Eq. 3 in the epilogue); a separate instantiation so the plain
-// prefill keeps its register allocation
-template <bool kCalib>
+// kMode 1, 2: fused calibration forward (Eq. 3 in the epilogue), 2 with d_alpha from d_o_hat; separate
+// instantiations so the plain prefill and the forward-only blend keep their own register allocation
+template <int kMode>
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
     prefill_tc_kernel(const __grid_constant__ PrefillParams p) {
+  constexpr bool kCalib = kMode >= 1, kDoHat = kMode == 2;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   if (sbase & 1023) __trap();  // SWIZZLE_128B tiles need a 1024-byte aligned base
@@ -735,17 +736,32 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       }
       // ---------------- epilogue: O / l -> global (this warp: O columns [128 ch, +128) = dims 256 ch + 128 kh ..)
       const uint32_t gl = g + U.n_tiles - 1;
-      // calibration with d_o_hat: this row's first d_o_hat chunk is requested before the wait for the last PV
-      const int64_t doff = ((int64_t)U.bi * p.o_sb + row_g * kDv + 256 * (int)ch + 128 * (int)kh) * 2;
-      const uint8_t* dhb = calib && p.d_o_hat ? p.d_o_hat + doff : nullptr;
-      const bool dload = calib && row_ok && dhb;
-      uint4 dn[4], dn2[4];
-      if constexpr (calib) {
+      // calibration with d_o_hat: the warp's 32 rows x 128 dims of d_o_hat are read coalesced (an instruction
+      // covers 4 rows x 128 B: lanes 8 j .. 8 j + 7 one row's 64 dims) and transposed through the idle P buffer
+      // (4 KB per warp) into this thread's row; the first 64 dims are requested before the wait for the last PV
+      // (per-thread row reads touched 32 rows, i.e. 32 L1 wavefronts, per instruction)
+      const int64_t rows_all = (int64_t)p.n_q * p.heads;
+      const int64_t drow0 = U.row0 + 64 * rank + 32 * (wq & 1);  // the warp's first row
+      const uint8_t* dbase = kDoHat
+                                 ? p.d_o_hat + ((int64_t)U.bi * p.o_sb + 256 * (int)ch + 128 * (int)kh) * 2 + 16 * (lane & 7)
+                                 : nullptr;
+      const uint32_t dscr = sbase + kOffP + (warp - 2) * 4096;  // this warp's transpose scratch
+      uint4 dl[8];
+      auto dload_pair = [&](int pp) {  // dims 64 pp .. 64 pp + 63 of the warp's 128, rows drow0 + 4 i + lane / 8
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dn[q] = dload ? ldg_nc_v4(dhb + 16 * q) : make_uint4(0, 0, 0, 0);
+        for (int i = 0; i < 8; ++i) {
+          const int64_t rg = drow0 + 4 * i + (lane >> 3);
+          dl[i] = dbase && rg < rows_all ? ldg_nc_v4(dbase + rg * kDv * 2 + 128 * pp) : make_uint4(0, 0, 0, 0);
+        }
+      };
+      auto dstage = [&]() {  // row 4 i + lane / 8 of the scratch, 16-B unit lane % 8 (swizzled by row & 7)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dn2[q] = dload ? ldg_nc_v4(dhb + 64 + 16 * q) : make_uint4(0, 0, 0, 0);
-      }
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t rl = 4 * i + (lane >> 3);
+          st_shared_v4(dscr + rl * 128 + ((((uint32_t)lane & 7) ^ (rl & 7)) << 4), dl[i].x, dl[i].y, dl[i].z, dl[i].w);
+        }
+      };
+      if constexpr (kDoHat) dload_pair(0);
       mbar_wait(bar(kBarOFull + (gl & 1)), (gl >> 1) & 1);
       tc_fence_after();
       float* ls = red + ((gl + 1) & 1) * 256;  // the exchange buffer not used by the last tile
@@ -779,22 +795,29 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           // d_alpha += d_o_hat (O - O'). O and d_o_hat are read straight from global (bf16, 64 B per chunk).
           float gs = 0.f;
           mbar_wait(bar(kBarOfFull), uc & 1);  // this unit's O_full rows, staged in the Q region
-          // d_o_hat chunks are software-pipelined one chunk ahead (chunk 0 was requested before the last PV's
-          // wait): the loads of chunk c + 1 are in flight while chunk c is converted (the TMEM wait's memory
-          // clobber would otherwise serialise 4 L2 latencies)
+          if constexpr (kDoHat) {  // dims 0-63 into the scratch, then the loads of dims 64-127
+            dstage();
+            __syncwarp();
+            dload_pair(1);
+          }
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t ov[32];
             tmem_ld32(taddr + kTmemO + 128 * ch + 32 * c, ov);
             uint32_t xw[16], dw[16];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              dw[4 * q] = dn[q].x; dw[4 * q + 1] = dn[q].y; dw[4 * q + 2] = dn[q].z; dw[4 * q + 3] = dn[q].w;
+            if (kDoHat && c == 2) {  // every lane has read dims 0-63 of its row: dims 64-127 into the scratch
+              __syncwarp();
+              dstage();
+              __syncwarp();
             }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {  // two chunks ahead
-              dn[q] = dn2[q];
-              if (c < 2) dn2[q] = dload ? ldg_nc_v4(dhb + 64 * (c + 2) + 16 * q) : make_uint4(0, 0, 0, 0);
+            for (int q = 0; q < 4; ++q) {  // this row's 32 dims of chunk c: units 4 (c & 1) .. of its scratch row
+              uint4 x4 = make_uint4(0, 0, 0, 0);
+              if (kDoHat)
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(x4.x), "=r"(x4.y), "=r"(x4.z), "=r"(x4.w)
+                             : "r"(dscr + (uint32_t)lane * 128 + ((((uint32_t)(4 * (c & 1) + q)) ^ ((uint32_t)lane & 7)) << 4)));
+              dw[4 * q] = x4.x; dw[4 * q + 1] = x4.y; dw[4 * q + 2] = x4.z; dw[4 * q + 3] = x4.w;
             }
             // O_full box m = dims [64 m, +64): row r at m * 8192 + 128 r, 16-B units swizzled by r & 7
             const uint8_t* ofs = smem + kOffQ + of_slot(4 * ch + 2 * kh + (c >> 1)) * 8192 + r * 128;
@@ -814,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
               const float y0 = __uint_as_float(ov[2 * j]) * inv, y1 = __uint_as_float(ov[2 * j + 1]) * inv;
               const float x0 = bf_lo(xw[j]), x1 = bf_hi(xw[j]);
               wc[j] = pack_bf16x2(fmaf(alpha, x0, om_alpha * y0), fmaf(alpha, x1, om_alpha * y1));
-              gs = fmaf(bf_lo(dw[j]), x0 - y0, fmaf(bf_hi(dw[j]), x1 - y1, gs));
+              if constexpr (kDoHat) gs = fmaf(bf_lo(dw[j]), x0 - y0, fmaf(bf_hi(dw[j]), x1 - y1, gs));
             }
 #pragma unroll
             for (int j = 0; j < 16; ++j) w[16 * c + j] = wc[j];
@@ -826,6 +849,7 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
         if (lane == 0) mbar_arrive_cluster(ofree);
         if (warp == 2 && lane == 0) TRACE(17, gl);
         const uint32_t stage = sbase + kOffP;
+        if constexpr (kDoHat) named_bar_sync(1, kSmThreads);  // every warp is done with its d_o_hat scratch
 #pragma unroll
         for (int rd = 0; rd < 2; ++rd) {  // round rd: the warps with ch == rd, dims [256 rd, +256) = 4 boxes
           if (rd == 1) {  // round 0's store reads the staging: decode the next unit meanwhile, then wait
@@ -968,19 +992,24 @@ cudaError_t launch_prefill_tc(const AttnProblem& a, cudaStream_t st) {
     if (!encode_4d_chunks(&p.v_map[i], s.v, kDv, len, a.batch, s.v_st, s.v_sb, kVKeys, 2)) return cudaErrorInvalidValue;
   }
   {  // per launch (the attribute is per device; a process may drive several GPUs)
-    cudaError_t e = a.calib ? cudaFuncSetAttribute(prefill_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   kSmemAlloc)
-                            : cudaFuncSetAttribute(prefill_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   kSmemAlloc);
+    const int mode = a.calib ? (a.calib->d_o_hat ? 2 : 1) : 0;
+    cudaError_t e = mode == 2   ? cudaFuncSetAttribute(prefill_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       kSmemAlloc)
+                    : mode == 1 ? cudaFuncSetAttribute(prefill_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       kSmemAlloc)
+                                : cudaFuncSetAttribute(prefill_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       kSmemAlloc);
     if (e != cudaSuccess) return e;
   }
   const int sms = device_sm_count();
   int64_t ncl = sms / 2;
   if (ncl > p.total_units) ncl = p.total_units;
-  if (a.calib)
-    prefill_tc_kernel<true><<<(unsigned)(2 * ncl), kThreads, kSmemAlloc, st>>>(p);
+  if (a.calib && a.calib->d_o_hat)
+    prefill_tc_kernel<2><<<(unsigned)(2 * ncl), kThreads, kSmemAlloc, st>>>(p);
+  else if (a.calib)
+    prefill_tc_kernel<1><<<(unsigned)(2 * ncl), kThreads, kSmemAlloc, st>>>(p);
   else
-    prefill_tc_kernel<false><<<(unsigned)(2 * ncl), kThreads, kSmemAlloc, st>>>(p);
+    prefill_tc_kernel<0><<<(unsigned)(2 * ncl), kThreads, kSmemAlloc, st>>>(p);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && a.calib && a.calib->part)
