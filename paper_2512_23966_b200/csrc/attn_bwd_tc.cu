@@ -51,6 +51,7 @@ struct TcBwdParams {
   CUtensorMap o_map;  // dO: {64, n_q*H, 8, B}, box {64, 128, 2, 1}
   CUtensorMap k_map;  // {64, n_kv, 9, B}, box {64, 32, 9, 1}
   CUtensorMap q4_map, q1_map, o4_map;  // pair kernels: q / dO boxes {64, 64, 4 (q1: 1), 1}
+  CUtensorMap ds_map;                  // pair kernels: the dS row buffer {W slots, n_q*H rows, B}, box {64, 128, 1}
   const float* lse;
   const float* D;
   float* dk;
@@ -846,6 +847,9 @@ __global__ void __launch_bounds__(256, 1) bwd_key64_tc_kernel(const __grid_const
 // dK^T 3 x 128 + dP 2 x 64. SMEM: ring 3 x 32 KB, K tile 72 KB (dV: 9 chunks) or 64 KB (dK: V's 8), P / dS
 // 2 x 16 KB, staging 2 x 8 KB. Warps 0-7 P / dS and the epilogue (warp w: TMEM lane quarter w % 4, column half w / 4),
 // warp 8 TMA, warp 9 UMMA issue (leader) and TMEM allocation, warp 10 the DSMEM copy.
+#ifndef PAIR_DS_TMA
+#define PAIR_DS_TMA 1
+#endif
 #ifndef BWD_DK_G2_M128
 #define BWD_DK_G2_M128 1
 #endif
@@ -870,7 +874,7 @@ struct PairCfg {
   static constexpr int kBarFull = 0, kBarEmpty = kStages, kBarK = 2 * kStages, kBarSFull = kBarK + 1,
                        kBarSFree = kBarSFull + kSBufs, kBarPLocal = kBarSFree + kSBufs, kBarPStaged = kBarPLocal + 2,
                        kBarPRecv = kBarPStaged + 2, kBarPFull = kBarPRecv + 2, kBarPFree = kBarPFull + 2,
-                       kBarAcc = kBarPFree + 2, kNumBars = kBarAcc + 1;
+                       kBarPStored = kBarPFree + 2, kBarAcc = kBarPStored + 2, kNumBars = kBarAcc + 1;
   static constexpr int kOffTmemPtr = kOffBar + 8 * kNumBars;
   static constexpr int kSmem = kOffTmemPtr + 16 + 1024;
   static constexpr int kFirstItems = kDv ? 3 : 2;  // Q (chunks 0-3, 4-7, 8) or dO (0-3, 4-7) of this CTA's 64 rows
@@ -948,6 +952,13 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
     p.trace[(int64_t)pc * 2] = g;
   }
+  // the tile's P / dS rows go to the dS row buffer by one TMA store of this CTA's key half (the operand buffer
+  // is already [128 rows][64 keys] swizzled, the box's layout) when all 128 rows are the segment's or the
+  // tensor ends inside the tile (the store clips there); otherwise by per-thread stores
+  const int rows_total = p.n_q * H;
+  auto tma_rows = [&](const RowIter& ri) {
+    return PAIR_DS_TMA && p.ds != nullptr && (ri.rb + kRows <= ri.re || ri.re == rows_total);
+  };
 
   auto bar = [&](int i) { return sbase + C::kOffBar + 8 * i; };
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + C::kOffTmemPtr);
@@ -967,6 +978,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       mbar_init(bar(C::kBarPRecv + i), 1);
       mbar_init(bar(C::kBarPFull + i), 2);  // the transfer warp of each CTA (leader's barrier)
       mbar_init(bar(C::kBarPFree + i), 1);
+      mbar_init(bar(C::kBarPStored + i), 1);  // the transfer warp: the TMA store of the tile's rows read P
     }
     mbar_init(bar(C::kBarAcc), 1);
     fence_mbar_init();
@@ -1155,9 +1167,20 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
           n2.advance();
           if (n2.valid()) mbar_arrive_expect_tx(bar(C::kBarPRecv + pb), C::kStBytes);  // tile tc + 2's, armed ahead
           mbar_arrive_release_cluster(pfull0 + 8 * pb);
+          if (tma_rows(ix)) {  // this CTA's 64 keys of the tile's 128 rows, from the complete operand buffer
+            const int t0 = div_h(p, ix.rb), QB = (p.q_start + t0) / p.b;
+            int lbq = QB - p.l + 1;
+            if (lbq < p.s) lbq = p.s;
+            const int slot = (kb < p.s ? j0 : p.s * p.b + (kb - lbq) * p.b) + 64 * (int)rank;
+            tma_store_3d(&p.ds_map, sbase + C::kOffP + pb * C::kPBytes, slot, ix.rb, bi);
+            bulk_commit_group();
+            bulk_wait_group_read0();
+          }
+          mbar_arrive_local(bar(C::kBarPStored + pb));  // buffer pb may take tile tc + 2
         }
         __syncwarp();
       }
+      if (lane == 0) bulk_wait_group0();
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------------ P or dS (thread = row x 32 keys)
@@ -1178,6 +1201,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       int pos;
       float lse2, Dr;
       uint4* ds;  // this row's 32 slots (keys jk ..) of block kb in the dS row buffer
+      bool tma;   // the tile's rows are written by the transfer warp's TMA store
     };
     auto row_in = [&](const RowIter& ri) {
       RowIn x;
@@ -1189,6 +1213,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       x.Dr = (!kDvK && x.rv) ? p.D[(int64_t)bi * rows + rr] : 0.f;
       x.win = jsink || kb >= x.pos / p.b - p.l + 1;
       x.ds = nullptr;
+      x.tma = tma_rows(ri);
       if (p.ds && x.rv) {
         int lbq = x.pos / p.b - p.l + 1;
         if (lbq < p.s) lbq = p.s;
@@ -1255,6 +1280,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
       if (warp == 0) BTRACE(8, tc);
       const int pb = tc & 1;
       mbar_wait(bar(C::kBarPFree + pb), ((tc >> 1) & 1) ^ 1);  // buffer pb's last gradient UMMAs (tile tc - 2) ran
+      mbar_wait(bar(C::kBarPStored + pb), ((tc >> 1) & 1) ^ 1);  // and the TMA store of tile tc - 2's rows read it
       if (warp == 0) BTRACE(9, tc);
       // row of 128 B = 8 x 16-B units (this thread's: 4 c .. 4 c + 3), SWIZZLE_128B: unit u at (u ^ row & 7)
 #pragma unroll
@@ -1269,7 +1295,7 @@ __global__ void __launch_bounds__(kPThreads, 1) __cluster_dims__(2, 1, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) prev_ds[u] = make_uint4(prev[4 * u], prev[4 * u + 1], prev[4 * u + 2], prev[4 * u + 3]);
       }
-      prev_ds = cur.ds;
+      prev_ds = cur.tma ? nullptr : cur.ds;
 #pragma unroll
       for (int u = 0; u < 16; ++u) prev[u] = pk[u];
       it = nx;
@@ -1936,6 +1962,11 @@ static cudaError_t launch_bwd_pair_tc(const AttnProblem& a, const void* dout, fl
   pk = p;
   pk.k_map = k8;
   pk.trace = g_bwd_trace_mode == kPairDk ? g_bwd_trace : nullptr;
+  {  // the dS row buffer as TMA store target: {W slots, rows, B}, box {64 slots, 128 rows, 1}, SW128
+    const int W = (a.s + a.l) * a.b;
+    if (!encode_3d(&p.ds_map, ds, (uint64_t)W, rows, a.batch, W, (int64_t)rows * W, kRows)) return cudaErrorInvalidValue;
+    pk.ds_map = p.ds_map;
+  }
   // the dK kernel's q1 box: [1 chunk][128 rows] (dK^T's third dim group)
   if (!encode_4d_chunks(&pk.q1_map, a.q, kDqk, rows, a.batch, a.q_sh, a.q_sb, kRows, 1)) return cudaErrorInvalidValue;
   const int64_t kt = (a.n_kv + kPKeys - 1) / kPKeys;
