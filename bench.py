@@ -466,7 +466,7 @@ def extra_rows(args, q, kv, o, flush, peaks):
     oh = torch.empty_like(of)
     dal = torch.empty(1, dtype=torch.float64, device=dev)
     t_full = _time_events(lambda: loza.full_attn_ref(q8, kv8, scale=scale, out=of), 3, 1, flush)
-    t_ssa = _time_events(lambda: loza.ssa_prefill(q8, kv8, pattern=PATTERN, scale=scale, out=osp), 5, 2, flush)
+    t_ssa = _time_events(lambda: loza.ssa_prefill(q8, kv8, pattern=PATTERN, scale=scale, out=osp), 10, 2, flush)
     t_bl = _time_events(lambda: loza.loza_blend(of, osp, alpha, dh, out=oh, d_alpha=dal), 10, 3, flush)
     bl_bytes = of.numel() * 2 * 4
     out["blend_8k"] = {"full_ms": float(np.mean(t_full)), "ssa_ms": float(np.mean(t_ssa)),
@@ -479,9 +479,9 @@ def extra_rows(args, q, kv, o, flush, peaks):
                        / peaks["bf16_tflops"]}
     # fused calibration forward: SSA + Eq. 3 + d_alpha in one kernel (O' never stored)
     t_fu = _time_events(lambda: loza.ssa_prefill_blend(q8, kv8, of, alpha, dh, pattern=PATTERN, scale=scale, out=oh),
-                        5, 2, flush)
+                        10, 2, flush)
     t_ff = _time_events(lambda: loza.ssa_prefill_blend(q8, kv8, of, alpha, pattern=PATTERN, scale=scale, out=oh),
-                        5, 2, flush)
+                        10, 2, flush)
     t_bf = _time_events(lambda: loza.loza_blend(of, osp, alpha, out=oh), 10, 3, flush)
     fu_ms = float(np.mean(t_fu))
     out["calibration_fused_8k"] = {
