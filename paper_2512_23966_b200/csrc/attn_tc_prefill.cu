@@ -764,6 +764,11 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
       if constexpr (kDoHat) dload_pair(0);
       mbar_wait(bar(kBarOFull + (gl & 1)), (gl >> 1) & 1);
       tc_fence_after();
+      if constexpr (kDoHat) {  // the P buffer is free: dims 0-63 into the scratch, then the loads of dims 64-127
+        dstage();
+        __syncwarp();
+        dload_pair(1);
+      }
       float* ls = red + ((gl + 1) & 1) * 256;  // the exchange buffer not used by the last tile
       ls[q4 * 64 + r] = lrow;
       named_bar_sync(1, kSmThreads);
@@ -795,11 +800,6 @@ __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(2, 1, 1)
           // d_alpha += d_o_hat (O - O'). O and d_o_hat are read straight from global (bf16, 64 B per chunk).
           float gs = 0.f;
           mbar_wait(bar(kBarOfFull), uc & 1);  // this unit's O_full rows, staged in the Q region
-          if constexpr (kDoHat) {  // dims 0-63 into the scratch, then the loads of dims 64-127
-            dstage();
-            __syncwarp();
-            dload_pair(1);
-          }
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t ov[32];
